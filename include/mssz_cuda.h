@@ -1,0 +1,153 @@
+/* mssz_cuda.h — C-ABI of the B200-native MSz segmentation-correction loop.
+ *
+ * Drop-in boundary for the reference's hot path.  The reference exposes C++
+ * templates with no FFI layer; every entry point below replaces
+ * one of them with plain pointers and sizes:
+ *
+ *   mssz_cu_derive_edits_{f32,f64}
+ *       replaces  template<class T> EditSet<T> derive_edits(const GridTopology&,
+ *                   const T* original, const T* decompressed, double xi,
+ *                   const DeriveOptions<T>& = {}, EditStats* = nullptr)
+ *                 /root/reference/proj/core/include/mssz/edit_engine.hpp:183-186
+ *                 (implementation edit_engine.cpp:386-435).  Host buffers in,
+ *                 callee-allocated EditSet out (release with mssz_cu_free).
+ *   mssz_cu_derive_edits_into_{f32,f64}
+ *       same, caller-provided host output buffers (no allocation per call).
+ *   mssz_cu_derive_edits_device_{f32,f64}
+ *       same, device-resident inputs/outputs on a caller stream.
+ *   mssz_cu_compute_directions_{f32,f64}
+ *       replaces  compute_directions<T> (mss.hpp:44-50, mss.cpp:11-30); returns
+ *                 the reference's u64 asc/desc vertex ids.
+ *   mssz_cu_compute_labels
+ *       replaces  compute_labels (mss.hpp:58-60, mss.cpp:84-97).
+ *   mssz_cu_classify_critical
+ *       replaces  classify_critical (mss.hpp:52, mss.cpp:40-47).
+ *   mssz_cu_detect_false_critical_{f32,f64}
+ *       replaces  EditState<T>::detect_false_critical (edit_engine.hpp:100,
+ *                 edit_engine.cpp:134-158) for an (original, edited) pair.
+ *   mssz_cu_lower_step_{f32,f64}, mssz_cu_representable_floor_{f32,f64}
+ *       element-wise EditState<T>::lower_step (edit_engine.cpp:75-86) and
+ *       representable_floor (edit_engine.cpp:22-29).
+ *   mssz_cu_apply_edits_{f32,f64}
+ *       replaces  apply_edits<T> (edit_engine.hpp:188-190, edit_engine.cpp:437-450).
+ *
+ * Conventions (mirroring errors.hpp:9-16): every function returns 0 or the
+ * reference ErrKind value (2 usage, 3 io, 4 bound_violation, 5 non_convergence,
+ * 6 corrupt_archive, 7 internal) and sets a thread-local message readable with
+ * mssz_cu_last_error().  99 = CUDA runtime failure (no device, launch error).
+ * Grids are row-major with axis 0 fastest (grid.hpp:32-43); dims[2] is
+ * ignored when ndims == 2.  Vertex counts must be < 2^32 - 1 (device ids are
+ * u32; the reference caps at 2^40, grid.cpp:19 — larger grids are sharded).
+ * Calls are synchronous and blocking, like the reference.  There is NO CPU
+ * fallback: without a usable CUDA device every compute entry point fails with 99.
+ */
+#ifndef MSSZ_CUDA_H
+#define MSSZ_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MSSZ_CU_OK 0
+#define MSSZ_CU_ERR_USAGE 2
+#define MSSZ_CU_ERR_IO 3
+#define MSSZ_CU_ERR_BOUND_VIOLATION 4
+#define MSSZ_CU_ERR_NON_CONVERGENCE 5
+#define MSSZ_CU_ERR_CORRUPT_ARCHIVE 6
+#define MSSZ_CU_ERR_INTERNAL 7
+#define MSSZ_CU_ERR_CUDA 99
+
+/* Mirrors DeriveOptions<T> (edit_engine.hpp:70-82).  ExecPolicy becomes a
+ * device choice; on_batch becomes an optional host callback (debug/parity
+ * mode: the device loop then stops after every batch so the host can read g). */
+typedef struct mssz_cu_options {
+  uint64_t outer_cap;   /* default 1000 */
+  uint64_t subloop_cap; /* default 640, per run_subloop invocation */
+  uint64_t r_cap;       /* default 100000, per run_r_loop invocation */
+  int32_t force;        /* accept |f - fhat| > xi inputs */
+  int32_t device;       /* CUDA ordinal; -1 = current device */
+  void (*on_batch)(const void* g_host, uint64_t n, void* user); /* NULL = off */
+  void* on_batch_user;
+} mssz_cu_options;
+
+/* Mirrors EditStats (edit_engine.hpp:54-68) field for field, then adds the
+ * device-side timings/counters of the B200 engine. */
+typedef struct mssz_cu_stats {
+  uint64_t outer_iterations;
+  uint64_t c_passes;
+  uint64_t sub_iterations[4]; /* FPmax, FPmin, FNmax, FNmin */
+  uint64_t r_iterations;
+  uint64_t effective_edits;
+  uint64_t touched;
+  uint64_t input_bound_violations;
+  double direction_seconds; /* device time of full direction sweeps (CUDA events) */
+  double label_seconds;     /* device time of label passes (CUDA events) */
+  /* B200 extras */
+  double h2d_seconds;
+  double d2h_seconds;
+  double device_seconds; /* whole device-side correction, validation to compaction */
+  uint64_t label_passes;
+  uint64_t label_rounds;
+  uint64_t detect_sweeps;
+  uint64_t frontier_vertices; /* sum over batches of |S ∪ N(S)| re-evaluated */
+  uint64_t kernel_launches;   /* kernels launched by this call */
+} mssz_cu_stats;
+
+void mssz_cu_default_options(mssz_cu_options* opt);
+const char* mssz_cu_last_error(void);
+void mssz_cu_free(void* p);
+int mssz_cu_device_count(void);
+const char* mssz_cu_version(void);
+/* Frees the cached per-device workspace (device buffers, pinned staging). */
+int mssz_cu_release_workspace(int device);
+
+#define MSSZ_CU_DECLARE_TYPED(SUF, T)                                                         \
+  int mssz_cu_derive_edits_##SUF(int ndims, const uint64_t* dims, const T* original,          \
+                                 const T* decompressed, double xi, const mssz_cu_options* opt, \
+                                 uint64_t** indices_out, T** values_out, uint64_t* count_out,  \
+                                 mssz_cu_stats* stats_out);                                    \
+  int mssz_cu_derive_edits_into_##SUF(int ndims, const uint64_t* dims, const T* original,     \
+                                      const T* decompressed, double xi,                        \
+                                      const mssz_cu_options* opt, uint64_t* indices,           \
+                                      T* values, uint64_t capacity, uint64_t* count_out,       \
+                                      mssz_cu_stats* stats_out);                               \
+  int mssz_cu_derive_edits_device_##SUF(int ndims, const uint64_t* dims,                      \
+                                        const T* d_original, const T* d_decompressed,          \
+                                        double xi, const mssz_cu_options* opt,                 \
+                                        uint64_t* d_indices, T* d_values, uint64_t capacity,   \
+                                        uint64_t* count_out, mssz_cu_stats* stats_out,         \
+                                        void* cuda_stream);                                    \
+  int mssz_cu_compute_directions_##SUF(int ndims, const uint64_t* dims, const T* values,      \
+                                       uint64_t* asc, uint64_t* desc);                         \
+  int mssz_cu_compute_direction_codes_##SUF(int ndims, const uint64_t* dims, const T* values, \
+                                            uint8_t* codes);                                   \
+  int mssz_cu_detect_false_critical_##SUF(int ndims, const uint64_t* dims, const T* original, \
+                                          const T* edited, uint64_t counts[4],                 \
+                                          uint64_t* lists);                                    \
+  int mssz_cu_detect_kind_##SUF(int ndims, const uint64_t* dims, const T* original,           \
+                                const T* edited, int kind, uint64_t* list,                     \
+                                uint64_t* count_out);                                          \
+  int mssz_cu_lower_step_##SUF(uint64_t n, const T* g, const T* f, double xi, T* g_out,       \
+                               uint8_t* moved);                                                \
+  int mssz_cu_representable_floor_##SUF(uint64_t n, const T* f, double xi, T* out);           \
+  int mssz_cu_apply_edits_##SUF(uint64_t n, const T* decompressed, const uint64_t* indices,   \
+                                const T* values, uint64_t count, T* out);
+
+MSSZ_CU_DECLARE_TYPED(f32, float)
+MSSZ_CU_DECLARE_TYPED(f64, double)
+
+/* asc/desc/labels are the reference's u64 vertex ids (mss.hpp:24-42). */
+int mssz_cu_compute_labels(int ndims, const uint64_t* dims, const uint64_t* asc,
+                           const uint64_t* desc, uint64_t* max_label, uint64_t* min_label);
+/* maxima/minima: caller buffers of n entries; counts out; sorted ascending. */
+int mssz_cu_classify_critical(uint64_t n, const uint64_t* asc, const uint64_t* desc,
+                              uint64_t* maxima, uint64_t* n_max, uint64_t* minima,
+                              uint64_t* n_min);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MSSZ_CUDA_H */

@@ -1,0 +1,493 @@
+"""mssz-b200: B200-native MSz segmentation-correction loop (arXiv 2406.09423).
+
+Python host mirror of the reference's ``proj/core`` hot-path API
+(``edit_engine.hpp``, ``mss.hpp``, ``grid.hpp``, ``errors.hpp``) over the
+C-ABI in ``include/mssz_cuda.h``.  Names, argument meaning and error kinds
+follow the reference so callers (and the parity tests) read like the
+reference's own:
+
+    topo  = build_topology([512, 512])                       # grid.hpp:51
+    edits = derive_edits(topo, f, fhat, xi, DeriveOptions(), stats)  # edit_engine.hpp:183
+    g     = apply_edits(topo, fhat, edits)                    # edit_engine.hpp:188
+
+Every compute entry point runs on the GPU through ``_lib/libmssz_b200.so``;
+there is no CPU fallback — without the built library or a CUDA device the
+calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from enum import IntEnum
+from typing import Callable, Optional
+
+import numpy as np
+
+from .build import CUDA_SO, INPUTS_SO, build  # noqa: F401
+
+__all__ = [
+    "ErrKind", "Error", "GridTopology", "build_topology", "DeriveOptions", "EditStats",
+    "EditSet", "DirectionField", "SegmentationLabels", "CriticalSet", "FalseCriticalReport",
+    "derive_edits", "derive_edits_into", "derive_edits_device", "compute_directions",
+    "compute_direction_codes", "compute_labels", "classify_critical", "detect_false_critical",
+    "detect_kind", "lower_step", "representable_floor", "apply_edits", "segmentation_equal",
+    "library", "build",
+]
+
+FPMAX, FPMIN, FNMAX, FNMIN = 0, 1, 2, 3
+
+
+class ErrKind(IntEnum):
+    """errors.hpp:9-16 (1:1 with CLI exit codes)."""
+
+    usage = 2
+    io = 3
+    bound_violation = 4
+    non_convergence = 5
+    corrupt_archive = 6
+    internal = 7
+    cuda = 99
+
+
+class Error(RuntimeError):
+    """errors.hpp:18-28 — ``kind()`` and ``exit_code()`` as in the reference."""
+
+    def __init__(self, kind: int, msg: str):
+        super().__init__(msg)
+        try:
+            self._kind = ErrKind(kind)
+        except ValueError:
+            self._kind = ErrKind.internal
+        self.msg = msg
+
+    def kind(self) -> ErrKind:
+        return self._kind
+
+    def exit_code(self) -> int:
+        return int(self._kind)
+
+
+# ---------------------------------------------------------------- topology
+_MAX_VERTICES = 1 << 40  # grid.cpp:19
+
+
+@dataclass(frozen=True)
+class GridTopology:
+    """grid.hpp:25-47 (row-major, axis 0 fastest; dims[2] == 1 in 2D)."""
+
+    ndims: int
+    dims: tuple
+    vertex_count: int
+
+    def coords_of(self, v: int):
+        x = v % self.dims[0]
+        y = (v // self.dims[0]) % self.dims[1]
+        z = v // (self.dims[0] * self.dims[1])
+        return x, y, z
+
+    def index_of(self, x: int, y: int, z: int = 0) -> int:
+        return x + self.dims[0] * (y + self.dims[1] * z)
+
+    @property
+    def extents(self):
+        return list(self.dims[: self.ndims])
+
+
+def build_topology(dims) -> GridTopology:
+    """build_topology (grid.cpp:39-55): usage error on bad extents."""
+    dims = [int(d) for d in dims]
+    if len(dims) not in (2, 3):
+        raise Error(ErrKind.usage, "dims must have 2 or 3 extents")
+    count = 1
+    for d in dims:
+        if d < 2:
+            raise Error(ErrKind.usage, "every grid extent must be >= 2")
+        if d > _MAX_VERTICES // count:
+            raise Error(ErrKind.usage, "grid exceeds the address-space cap")
+        count *= d
+    full = tuple(dims + [1] * (3 - len(dims)))
+    return GridTopology(len(dims), full, count)
+
+
+# ---------------------------------------------------------------- results
+@dataclass
+class DeriveOptions:
+    """DeriveOptions<T> (edit_engine.hpp:70-82); ``device`` replaces ExecPolicy."""
+
+    outer_cap: int = 1000
+    subloop_cap: int = 640
+    r_cap: int = 100000
+    force: bool = False
+    device: int = -1
+    on_batch: Optional[Callable[[np.ndarray], None]] = None
+
+
+@dataclass
+class EditStats:
+    """EditStats (edit_engine.hpp:54-68) plus the device counters."""
+
+    outer_iterations: int = 0
+    c_passes: int = 0
+    sub_iterations: list = field(default_factory=lambda: [0, 0, 0, 0])
+    r_iterations: int = 0
+    effective_edits: int = 0
+    touched: int = 0
+    input_bound_violations: int = 0
+    direction_seconds: float = 0.0
+    label_seconds: float = 0.0
+    h2d_seconds: float = 0.0
+    d2h_seconds: float = 0.0
+    device_seconds: float = 0.0
+    label_passes: int = 0
+    label_rounds: int = 0
+    detect_sweeps: int = 0
+    frontier_vertices: int = 0
+    kernel_launches: int = 0
+
+    def sub_iterations_total(self) -> int:
+        return sum(self.sub_iterations)
+
+
+@dataclass
+class EditSet:
+    """EditSet<T> (edit_engine.hpp:45-52): strictly increasing indices, absolute values."""
+
+    indices: np.ndarray
+    values: np.ndarray
+
+    def size(self) -> int:
+        return int(self.indices.size)
+
+    def empty(self) -> bool:
+        return self.indices.size == 0
+
+
+@dataclass
+class DirectionField:
+    """mss.hpp:24-31."""
+
+    asc: np.ndarray
+    desc: np.ndarray
+
+    def is_max(self, v: int) -> bool:
+        return int(self.asc[v]) == v
+
+    def is_min(self, v: int) -> bool:
+        return int(self.desc[v]) == v
+
+
+@dataclass
+class SegmentationLabels:
+    """mss.hpp:37-42."""
+
+    max_label: np.ndarray
+    min_label: np.ndarray
+
+    def __eq__(self, other) -> bool:
+        return bool(np.array_equal(self.max_label, other.max_label)
+                    and np.array_equal(self.min_label, other.min_label))
+
+
+@dataclass
+class CriticalSet:
+    """mss.hpp:32-35."""
+
+    maxima: np.ndarray
+    minima: np.ndarray
+
+
+@dataclass
+class FalseCriticalReport:
+    """edit_engine.hpp:29-41 (first matching class wins)."""
+
+    fp_max: np.ndarray
+    fp_min: np.ndarray
+    fn_max: np.ndarray
+    fn_min: np.ndarray
+
+    def empty(self) -> bool:
+        return self.total() == 0
+
+    def total(self) -> int:
+        return int(self.fp_max.size + self.fp_min.size + self.fn_max.size + self.fn_min.size)
+
+
+# ---------------------------------------------------------------- C-ABI
+class _Options(C.Structure):
+    _fields_ = [
+        ("outer_cap", C.c_uint64), ("subloop_cap", C.c_uint64), ("r_cap", C.c_uint64),
+        ("force", C.c_int32), ("device", C.c_int32),
+        ("on_batch", C.c_void_p), ("on_batch_user", C.c_void_p),
+    ]
+
+
+class _Stats(C.Structure):
+    _fields_ = [
+        ("outer_iterations", C.c_uint64), ("c_passes", C.c_uint64),
+        ("sub_iterations", C.c_uint64 * 4), ("r_iterations", C.c_uint64),
+        ("effective_edits", C.c_uint64), ("touched", C.c_uint64),
+        ("input_bound_violations", C.c_uint64), ("direction_seconds", C.c_double),
+        ("label_seconds", C.c_double), ("h2d_seconds", C.c_double),
+        ("d2h_seconds", C.c_double), ("device_seconds", C.c_double),
+        ("label_passes", C.c_uint64), ("label_rounds", C.c_uint64),
+        ("detect_sweeps", C.c_uint64), ("frontier_vertices", C.c_uint64),
+        ("kernel_launches", C.c_uint64),
+    ]
+
+    def fill(self, st: EditStats) -> EditStats:
+        for name, _ in self._fields_:
+            v = getattr(self, name)
+            setattr(st, name, list(v) if name == "sub_iterations" else v)
+        return st
+
+
+_BATCH_CB = C.CFUNCTYPE(None, C.c_void_p, C.c_uint64, C.c_void_p)
+
+# every symbol include/mssz_cuda.h declares (tests check the exports)
+EXPORTS = [
+    "mssz_cu_default_options", "mssz_cu_last_error", "mssz_cu_free", "mssz_cu_device_count",
+    "mssz_cu_version", "mssz_cu_release_workspace", "mssz_cu_compute_labels",
+    "mssz_cu_classify_critical",
+] + [
+    f"mssz_cu_{name}_{suf}" for suf in ("f32", "f64") for name in (
+        "derive_edits", "derive_edits_into", "derive_edits_device", "compute_directions",
+        "compute_direction_codes", "detect_false_critical", "detect_kind", "lower_step",
+        "representable_floor", "apply_edits")
+]
+
+_lib = None
+
+
+def library() -> C.CDLL:
+    """Loads ``_lib/libmssz_b200.so`` (fails loudly when it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(CUDA_SO):
+            raise Error(ErrKind.cuda, f"CUDA extension missing: {CUDA_SO} (run build())")
+        lib = C.CDLL(CUDA_SO)
+        lib.mssz_cu_last_error.restype = C.c_char_p
+        lib.mssz_cu_version.restype = C.c_char_p
+        lib.mssz_cu_free.argtypes = [C.c_void_p]
+        _lib = lib
+    return _lib
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        raise Error(rc, library().mssz_cu_last_error().decode())
+
+
+def _suf(dtype) -> str:
+    dt = np.dtype(dtype)
+    if dt == np.float32:
+        return "f32"
+    if dt == np.float64:
+        return "f64"
+    raise Error(ErrKind.usage, f"unsupported dtype {dt} (f32 or f64)")
+
+
+def _ctype(dtype):
+    return C.c_float if np.dtype(dtype) == np.float32 else C.c_double
+
+
+def _dims(topo: GridTopology):
+    return (C.c_uint64 * 3)(*topo.dims)
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _field(topo: GridTopology, a, name: str, dtype=None) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=dtype)
+    if a.size != topo.vertex_count:
+        raise Error(ErrKind.io, f"{name}: {a.size} values for a grid of {topo.vertex_count}")
+    return a.reshape(-1)
+
+
+def _options(opts: Optional[DeriveOptions], dtype, keep: list) -> _Options:
+    o = opts or DeriveOptions()
+    co = _Options(o.outer_cap, o.subloop_cap, o.r_cap, int(o.force), o.device, None, None)
+    if o.on_batch is not None:
+        ctype = _ctype(dtype)
+
+        def _cb(ptr, n, user):
+            arr = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(ctype)), shape=(n,))
+            o.on_batch(arr.copy())
+
+        cb = _BATCH_CB(_cb)
+        keep.append(cb)
+        co.on_batch = C.cast(cb, C.c_void_p)
+    return co
+
+
+def derive_edits(topo: GridTopology, original, decompressed, xi: float,
+                 opts: Optional[DeriveOptions] = None,
+                 stats: Optional[EditStats] = None) -> EditSet:
+    """derive_edits<T> (edit_engine.hpp:183-186) on the GPU; host arrays in, EditSet out."""
+    f = _field(topo, original, "original")
+    fh = _field(topo, decompressed, "decompressed", f.dtype)
+    suf = _suf(f.dtype)
+    keep: list = []
+    co = _options(opts, f.dtype, keep)
+    idx = C.POINTER(C.c_uint64)()
+    val = C.POINTER(_ctype(f.dtype))()
+    count = C.c_uint64()
+    st = _Stats()
+    lib = library()
+    rc = getattr(lib, f"mssz_cu_derive_edits_{suf}")(
+        topo.ndims, _dims(topo), _p(f), _p(fh), C.c_double(xi), C.byref(co), C.byref(idx),
+        C.byref(val), C.byref(count), C.byref(st))
+    _check(rc)
+    k = count.value
+    indices = np.ctypeslib.as_array(idx, shape=(max(k, 1),))[:k].copy()
+    values = np.ctypeslib.as_array(val, shape=(max(k, 1),))[:k].copy()
+    lib.mssz_cu_free(C.cast(idx, C.c_void_p))
+    lib.mssz_cu_free(C.cast(val, C.c_void_p))
+    if stats is not None:
+        st.fill(stats)
+    return EditSet(indices, values)
+
+
+def derive_edits_into(topo: GridTopology, f_ptr: int, fh_ptr: int, xi: float, idx_ptr: int,
+                      val_ptr: int, capacity: int, dtype=np.float32,
+                      opts: Optional[DeriveOptions] = None) -> tuple:
+    """Host-pointer variant with caller-owned (e.g. pinned) output buffers -> (count, EditStats)."""
+    suf = _suf(dtype)
+    keep: list = []
+    co = _options(opts, dtype, keep)
+    count = C.c_uint64()
+    st = _Stats()
+    rc = getattr(library(), f"mssz_cu_derive_edits_into_{suf}")(
+        topo.ndims, _dims(topo), C.c_void_p(f_ptr), C.c_void_p(fh_ptr), C.c_double(xi),
+        C.byref(co), C.c_void_p(idx_ptr), C.c_void_p(val_ptr), C.c_uint64(capacity),
+        C.byref(count), C.byref(st))
+    _check(rc)
+    return count.value, st.fill(EditStats())
+
+
+def derive_edits_device(topo: GridTopology, d_f: int, d_fh: int, xi: float, d_idx: int,
+                        d_val: int, capacity: int, dtype=np.float32,
+                        opts: Optional[DeriveOptions] = None, stream: int = 0) -> tuple:
+    """Device-resident variant (CUDA pointers, optional stream) -> (count, EditStats)."""
+    suf = _suf(dtype)
+    keep: list = []
+    co = _options(opts, dtype, keep)
+    count = C.c_uint64()
+    st = _Stats()
+    rc = getattr(library(), f"mssz_cu_derive_edits_device_{suf}")(
+        topo.ndims, _dims(topo), C.c_void_p(d_f), C.c_void_p(d_fh), C.c_double(xi),
+        C.byref(co), C.c_void_p(d_idx), C.c_void_p(d_val), C.c_uint64(capacity),
+        C.byref(count), C.byref(st), C.c_void_p(stream or None))
+    _check(rc)
+    return count.value, st.fill(EditStats())
+
+
+def compute_directions(topo: GridTopology, values) -> DirectionField:
+    """compute_directions<T> (mss.hpp:44-50): u64 steepest neighbour ids, SELF = own id."""
+    v = _field(topo, values, "values")
+    asc = np.empty(topo.vertex_count, np.uint64)
+    desc = np.empty(topo.vertex_count, np.uint64)
+    _check(getattr(library(), f"mssz_cu_compute_directions_{_suf(v.dtype)}")(
+        topo.ndims, _dims(topo), _p(v), _p(asc), _p(desc)))
+    return DirectionField(asc, desc)
+
+
+def compute_direction_codes(topo: GridTopology, values) -> np.ndarray:
+    """Packed device representation: low nibble asc slot, high nibble desc slot, 15 = SELF."""
+    v = _field(topo, values, "values")
+    out = np.empty(topo.vertex_count, np.uint8)
+    _check(getattr(library(), f"mssz_cu_compute_direction_codes_{_suf(v.dtype)}")(
+        topo.ndims, _dims(topo), _p(v), _p(out)))
+    return out
+
+
+def compute_labels(topo: GridTopology, directions: DirectionField) -> SegmentationLabels:
+    """compute_labels (mss.hpp:58-60); raises internal on a corrupt (cyclic) field."""
+    asc = _field(topo, directions.asc, "asc", np.uint64)
+    desc = _field(topo, directions.desc, "desc", np.uint64)
+    M = np.empty(topo.vertex_count, np.uint64)
+    m = np.empty(topo.vertex_count, np.uint64)
+    _check(library().mssz_cu_compute_labels(topo.ndims, _dims(topo), _p(asc), _p(desc), _p(M),
+                                            _p(m)))
+    return SegmentationLabels(M, m)
+
+
+def classify_critical(directions: DirectionField) -> CriticalSet:
+    """classify_critical (mss.cpp:40-47): sorted maxima / minima."""
+    asc = np.ascontiguousarray(directions.asc, np.uint64)
+    desc = np.ascontiguousarray(directions.desc, np.uint64)
+    n = asc.size
+    mx = np.empty(n, np.uint64)
+    mn = np.empty(n, np.uint64)
+    nmx = C.c_uint64()
+    nmn = C.c_uint64()
+    _check(library().mssz_cu_classify_critical(C.c_uint64(n), _p(asc), _p(desc), _p(mx),
+                                               C.byref(nmx), _p(mn), C.byref(nmn)))
+    return CriticalSet(mx[: nmx.value].copy(), mn[: nmn.value].copy())
+
+
+def detect_false_critical(topo: GridTopology, original, edited) -> FalseCriticalReport:
+    """EditState::detect_false_critical (edit_engine.cpp:134-158) for (f, g)."""
+    f = _field(topo, original, "original")
+    g = _field(topo, edited, "edited", f.dtype)
+    n = topo.vertex_count
+    counts = np.zeros(4, np.uint64)
+    lists = np.zeros(4 * n, np.uint64)
+    _check(getattr(library(), f"mssz_cu_detect_false_critical_{_suf(f.dtype)}")(
+        topo.ndims, _dims(topo), _p(f), _p(g), _p(counts), _p(lists)))
+    parts = [lists[k * n: k * n + int(counts[k])].copy() for k in range(4)]
+    return FalseCriticalReport(*parts)
+
+
+def detect_kind(topo: GridTopology, original, edited, kind: int) -> np.ndarray:
+    """EditState::detect_kind (edit_engine.cpp:104-132): sorted, per kind, non-exclusive."""
+    f = _field(topo, original, "original")
+    g = _field(topo, edited, "edited", f.dtype)
+    out = np.empty(topo.vertex_count, np.uint64)
+    cnt = C.c_uint64()
+    _check(getattr(library(), f"mssz_cu_detect_kind_{_suf(f.dtype)}")(
+        topo.ndims, _dims(topo), _p(f), _p(g), int(kind), _p(out), C.byref(cnt)))
+    return out[: cnt.value].copy()
+
+
+def lower_step(g, f, xi: float):
+    """Element-wise EditState::lower_step (edit_engine.cpp:75-86) -> (new g, moved mask)."""
+    f = np.ascontiguousarray(f).reshape(-1)
+    g = np.ascontiguousarray(g, f.dtype).reshape(-1)
+    out = np.empty_like(g)
+    moved = np.empty(g.size, np.uint8)
+    _check(getattr(library(), f"mssz_cu_lower_step_{_suf(f.dtype)}")(
+        C.c_uint64(g.size), _p(g), _p(f), C.c_double(xi), _p(out), _p(moved)))
+    return out, moved.astype(bool)
+
+
+def representable_floor(f, xi: float) -> np.ndarray:
+    """Element-wise representable_floor (edit_engine.cpp:22-29)."""
+    f = np.ascontiguousarray(f).reshape(-1)
+    out = np.empty_like(f)
+    _check(getattr(library(), f"mssz_cu_representable_floor_{_suf(f.dtype)}")(
+        C.c_uint64(f.size), _p(f), C.c_double(xi), _p(out)))
+    return out
+
+
+def apply_edits(topo: GridTopology, decompressed, edits: EditSet) -> np.ndarray:
+    """apply_edits<T> (edit_engine.hpp:188-190); corrupt_archive on bad input."""
+    fh = _field(topo, decompressed, "decompressed")
+    if edits.indices.size != edits.values.size:
+        raise Error(ErrKind.corrupt_archive, "edit set index/value length mismatch")
+    idx = np.ascontiguousarray(edits.indices, np.uint64)
+    vals = np.ascontiguousarray(edits.values, fh.dtype)
+    out = np.empty_like(fh)
+    _check(getattr(library(), f"mssz_cu_apply_edits_{_suf(fh.dtype)}")(
+        C.c_uint64(fh.size), _p(fh), _p(idx), _p(vals), C.c_uint64(idx.size), _p(out)))
+    return out
+
+
+def segmentation_equal(a: SegmentationLabels, b: SegmentationLabels):
+    """segmentation_equal (mss.cpp:122-133) -> (match mask, mismatches)."""
+    if a.max_label.size != b.max_label.size:
+        raise Error(ErrKind.usage, "segmentation_equal: topology mismatch")
+    match = (a.max_label == b.max_label) & (a.min_label == b.min_label)
+    return match.astype(np.uint8), int(match.size - int(match.sum()))

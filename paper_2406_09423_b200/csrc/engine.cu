@@ -1,0 +1,1000 @@
+// Host engine + C-ABI of the B200 correction loop (include/mssz_cuda.h).
+//
+// derive_edits orchestration mirrors edit_engine.cpp:386-435 (validation,
+// EditState ctor, outer{C-loop; R-loop}, postcondition tripwire, edits()).
+// The host only sees one small control block per subloop / R iteration: every
+// detect → fix → refresh batch runs inside a cooperative persistent kernel.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/mssz_cuda.h"
+#include "kernels.cuh"
+
+namespace mssz_b200 {
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Fail {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  throw Fail{code, buf};
+}
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      fail(MSSZ_CU_ERR_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_),    \
+           __FILE__, __LINE__);                                                         \
+  } while (0)
+
+#define CK_LAUNCH() CK(cudaGetLastError())
+
+template <class F>
+int guarded(F&& body) {
+  try {
+    body();
+    g_last_error.clear();
+    return MSSZ_CU_OK;
+  } catch (const Fail& f) {
+    g_last_error = f.msg;
+    return f.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return MSSZ_CU_ERR_CUDA;
+  }
+}
+
+// Validates dims like build_topology (grid.cpp:39-55) plus the u32 id limit.
+Geom make_geom(int ndims, const uint64_t* dims) {
+  if (ndims != 2 && ndims != 3) fail(MSSZ_CU_ERR_USAGE, "dims must have 2 or 3 extents");
+  if (!dims) fail(MSSZ_CU_ERR_USAGE, "dims is null");
+  const uint64_t cap = uint64_t(1) << 40;
+  uint64_t count = 1;
+  uint64_t d[3] = {1, 1, 1};
+  for (int a = 0; a < ndims; ++a) {
+    if (dims[a] < 2) fail(MSSZ_CU_ERR_USAGE, "every grid extent must be >= 2");
+    if (dims[a] > cap / count) fail(MSSZ_CU_ERR_USAGE, "grid exceeds the address-space cap");
+    d[a] = dims[a];
+    count *= dims[a];
+  }
+  if (count >= 0xFFFFFFFFull)
+    fail(MSSZ_CU_ERR_USAGE,
+         "grid of %llu vertices exceeds the single-device u32 id space; shard it into z-slabs",
+         (unsigned long long)count);
+  Geom g{};
+  g.ndims = ndims;
+  g.nst = ndims == 2 ? 6 : 14;
+  g.X = static_cast<uint32_t>(d[0]);
+  g.Y = static_cast<uint32_t>(d[1]);
+  g.Z = static_cast<uint32_t>(d[2]);
+  g.XY = g.X * g.Y;
+  g.n = static_cast<uint32_t>(count);
+  for (int k = 0; k < 16; ++k) g.off[k] = 0;
+  for (int k = 0; k < g.nst; ++k) {
+    int dx, dy, dz;
+    if (ndims == 2) stencil<2>(k, dx, dy, dz);
+    else stencil<3>(k, dx, dy, dz);
+    g.off[k] = dx + dy * static_cast<int32_t>(g.X) + dz * static_cast<int32_t>(g.XY);
+  }
+  return g;
+}
+
+int bit_width_u64(uint64_t x) {
+  int w = 0;
+  while (x) {
+    ++w;
+    x >>= 1;
+  }
+  return w;
+}
+
+uint32_t grid_for(uint64_t work, int threads, int sms, int per_sm = 8) {
+  uint64_t b = (work + threads - 1) / threads;
+  const uint64_t cap = static_cast<uint64_t>(sms) * per_sm;
+  if (b > cap) b = cap;
+  if (b == 0) b = 1;
+  return static_cast<uint32_t>(b);
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  bool ensure(size_t bytes) {  // returns true when (re)allocated
+    if (bytes <= cap && p) return false;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    CK(cudaMalloc(&p, bytes ? bytes : 16));
+    cap = bytes;
+    return true;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  template <class U>
+  U* as() const {
+    return static_cast<U*>(p);
+  }
+};
+
+// Per-device cached workspace: device buffers grow monotonically, claim and
+// frontier stamp ids keep increasing across calls so the stamp arrays are only
+// cleared when (re)allocated.
+struct Workspace {
+  int device = 0;
+  int sms = 0;
+  cudaStream_t stream = nullptr;
+  DevBuf f, g, fdir, gdir, touched, stamp, fmark, lab, lists, tiles;
+  Ctl* ctl = nullptr;
+  Ctl* hctl = nullptr;  // pinned mirror
+  uint32_t next_batch = 1, next_mark = 1;
+  cudaEvent_t ev[4] = {};
+  std::mutex mu;
+  uint64_t launches = 0;
+
+  void init(int dev) {
+    device = dev;
+    CK(cudaSetDevice(dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    CK(cudaMalloc(&ctl, sizeof(Ctl)));
+    CK(cudaMallocHost(&hctl, sizeof(Ctl)));
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+  }
+  void release() {
+    for (DevBuf* b : {&f, &g, &fdir, &gdir, &touched, &stamp, &fmark, &lab, &lists, &tiles})
+      b->release();
+    next_batch = next_mark = 1;
+  }
+
+  // Sizes every buffer for n vertices of element size es.
+  void ensure(uint64_t n, size_t es) {
+    const uint64_t np = (n + 63) & ~uint64_t(63);
+    f.ensure(np * es);
+    g.ensure(np * es);
+    fdir.ensure(np);
+    gdir.ensure(np);
+    touched.ensure(np);
+    bool fresh = stamp.ensure(np * 4);
+    fresh |= fmark.ensure(np * 4);
+    lab.ensure(np * 16);    // fM fm gM gm (u32)
+    lists.ensure(np * 16);  // list0 list1 S F (u32); reused as the u64+T EditSet
+    tiles.ensure(((n + kCompactTile - 1) / kCompactTile + 1) * 4);
+    if (fresh || next_batch > 0xF0000000u || next_mark > 0xF0000000u) {
+      CK(cudaMemsetAsync(stamp.p, 0, stamp.cap, stream));
+      CK(cudaMemsetAsync(fmark.p, 0, fmark.cap, stream));
+      next_batch = next_mark = 1;
+    }
+  }
+
+  void push_ctl() { CK(cudaMemcpyAsync(ctl, hctl, sizeof(Ctl), cudaMemcpyHostToDevice, stream)); }
+  void pull_ctl() {
+    CK(cudaMemcpyAsync(hctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+  }
+  void sync() { CK(cudaStreamSynchronize(stream)); }
+};
+
+std::mutex g_ws_mu;
+std::vector<std::unique_ptr<Workspace>> g_ws;
+
+Workspace& workspace(int device) {
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    fail(MSSZ_CU_ERR_CUDA, "no CUDA device available (%s); the B200 engine has no CPU fallback",
+         e == cudaSuccess ? "0 devices" : cudaGetErrorString(e));
+  if (device < 0) CK(cudaGetDevice(&device));
+  if (device >= ndev) fail(MSSZ_CU_ERR_USAGE, "device %d out of range (%d devices)", device, ndev);
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  if (g_ws.size() < static_cast<size_t>(ndev)) g_ws.resize(ndev);
+  if (!g_ws[device]) {
+    auto ws = std::make_unique<Workspace>();
+    ws->init(device);
+    g_ws[device] = std::move(ws);
+  }
+  CK(cudaSetDevice(device));
+  return *g_ws[device];
+}
+
+const char* kKindName[4] = {"FPmax", "FPmin", "FNmax", "FNmin"};
+
+// ---------------------------------------------------------------------------
+template <class T>
+struct Engine {
+  Workspace& ws;
+  Geom geo;
+  mssz_cu_options opt;
+  mssz_cu_stats st{};
+  State<T> s{};
+  uint32_t cur = 0;
+  int coop_blocks = 0;
+  std::vector<T> host_g;  // on_batch snapshots only
+  float dir_ms = 0.f, lab_ms = 0.f;
+
+  Engine(Workspace& w, const Geom& g, const mssz_cu_options& o) : ws(w), geo(g), opt(o) {}
+
+  uint32_t n() const { return geo.n; }
+  uint32_t* list(int k) const { return ws.lists.as<uint32_t>() + static_cast<uint64_t>(k) * ((n() + 63) & ~63u); }
+  uint32_t* lab(int k) const { return ws.lab.as<uint32_t>() + static_cast<uint64_t>(k) * ((n() + 63) & ~63u); }
+
+  void bind(const T* d_f) {
+    s.geo = geo;
+    s.f = d_f;
+    s.g = ws.g.as<T>();
+    s.fdir = ws.fdir.as<uint8_t>();
+    s.gdir = ws.gdir.as<uint8_t>();
+    s.touched = ws.touched.as<uint8_t>();
+    s.stamp = ws.stamp.as<uint32_t>();
+    s.fmark = ws.fmark.as<uint32_t>();
+    s.list[0] = list(0);
+    s.list[1] = list(1);
+    s.S = list(2);
+    s.F = list(3);
+    s.fM = lab(0);
+    s.fm = lab(1);
+    s.gM = lab(2);
+    s.gm = lab(3);
+    s.xi = 0;
+    s.ctl = ws.ctl;
+  }
+
+  void launched() {
+    ++ws.launches;
+    ++st.kernel_launches;
+    CK_LAUNCH();
+  }
+
+  void directions(const T* vals, uint8_t* dir) {
+    dim3 block(128), grid((geo.X + 127) / 128, geo.Y, geo.Z);
+    if (geo.ndims == 2) k_directions<T, 2><<<grid, block, 0, ws.stream>>>(vals, dir, geo);
+    else k_directions<T, 3><<<grid, block, 0, ws.stream>>>(vals, dir, geo);
+    launched();
+  }
+
+  // Pointer-jumping labels; M/m already initialised (codes: k_label_init).
+  // Rounds are launched in groups of 4 and the group's last flag is read back.
+  void jump_to_fixpoint(uint32_t* M, uint32_t* m) {
+    const int cap = bit_width_u64(static_cast<uint64_t>(n()) - 1) + 2;
+    const uint32_t blocks = grid_for(n(), 256, ws.sms, 16);
+    int round = 0;
+    for (;;) {
+      const int group = 4;
+      CK(cudaMemsetAsync(ws.ctl->flags, 0, sizeof(uint32_t) * group, ws.stream));
+      for (int r = 0; r < group; ++r) {
+        k_label_jump<<<blocks, 256, 0, ws.stream>>>(M, m, n(), &ws.ctl->flags[r]);
+        launched();
+      }
+      uint32_t flags[4];
+      CK(cudaMemcpyAsync(flags, ws.ctl->flags, sizeof flags, cudaMemcpyDeviceToHost, ws.stream));
+      ws.sync();
+      int used = 0;
+      while (used < group && flags[used]) ++used;
+      round += used;
+      st.label_rounds += used < group ? used + 1 : used;
+      if (used < group) return;  // a round observed the fixpoint
+      if (round > cap)
+        fail(MSSZ_CU_ERR_INTERNAL,
+             "path compression exceeded its round cap (corrupt direction field)");
+    }
+  }
+
+  void labels_from_codes(const uint8_t* dir, uint32_t* M, uint32_t* m) {
+    CK(cudaEventRecord(ws.ev[2], ws.stream));
+    k_label_init<<<grid_for(n(), 256, ws.sms, 16), 256, 0, ws.stream>>>(dir, geo, M, m);
+    launched();
+    jump_to_fixpoint(M, m);
+    CK(cudaEventRecord(ws.ev[3], ws.stream));
+    CK(cudaEventSynchronize(ws.ev[3]));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, ws.ev[2], ws.ev[3]));
+    lab_ms += ms;
+    ++st.label_passes;
+  }
+
+  void reset_ctl() {
+    std::memset(ws.hctl, 0, sizeof(Ctl));
+    ws.hctl->cur = cur;
+  }
+
+  int coop_grid() {
+    if (coop_blocks) return coop_blocks;
+    int occ = 0;
+    if (geo.ndims == 2)
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subloop<T, 2>, 512, 0));
+    else
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subloop<T, 3>, 512, 0));
+    if (occ < 1) fail(MSSZ_CU_ERR_CUDA, "persistent subloop kernel cannot be co-resident");
+    coop_blocks = ws.sms * std::min(occ, 2);
+    return coop_blocks;
+  }
+
+  void on_batch() {
+    if (!opt.on_batch) return;
+    host_g.resize(n());
+    CK(cudaMemcpyAsync(host_g.data(), s.g, sizeof(T) * n(), cudaMemcpyDeviceToHost, ws.stream));
+    ws.sync();
+    opt.on_batch(host_g.data(), n(), opt.on_batch_user);
+  }
+
+  // run_subloop (edit_engine.cpp:246-278)
+  uint64_t run_subloop(int kind) {
+    reset_ctl();
+    ws.push_ctl();
+    k_detect_kind<<<grid_for((n() + 15) / 16, 256, ws.sms, 16), 256, 0, ws.stream>>>(
+        s.fdir, s.gdir, n(), kind, s.list[cur], &ws.ctl->list_count[cur]);
+    launched();
+    ++st.detect_sweeps;
+    const uint32_t batch_base = ws.next_batch, mark_base = ws.next_mark;
+    uint64_t cap = opt.subloop_cap;
+    uint32_t maxb = opt.on_batch ? 1u : 0xFFFFFFFFu;
+    void* args[] = {&s, &kind, &cap, (void*)&batch_base, (void*)&mark_base, &maxb};
+    void* fn = geo.ndims == 2 ? (void*)k_subloop<T, 2> : (void*)k_subloop<T, 3>;
+    const int blocks = coop_grid();
+    uint64_t seen_iters = 0;
+    for (;;) {
+      CK(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(512), args, 0, ws.stream));
+      launched();
+      ws.pull_ctl();
+      const Ctl& c = *ws.hctl;
+      if (!opt.on_batch || c.status != kStatusOk) break;
+      if (c.iters == seen_iters) break;  // list empty
+      seen_iters = c.iters;
+      on_batch();
+    }
+    const Ctl& c = *ws.hctl;
+    cur = c.cur;
+    ws.next_batch += static_cast<uint32_t>(2 * c.attempted + 4);
+    ws.next_mark += static_cast<uint32_t>(c.attempted + 2);
+    if (c.status == kStatusCap)
+      fail(MSSZ_CU_ERR_NON_CONVERGENCE, "%s subloop exceeded its iteration cap", kKindName[kind]);
+    if (c.status == kStatusStall)
+      fail(MSSZ_CU_ERR_NON_CONVERGENCE, "%s subloop stalled at the float floor", kKindName[kind]);
+    st.sub_iterations[kind] += c.iters;
+    st.effective_edits += c.edits;
+    st.frontier_vertices += c.frontier;
+    return c.edits;
+  }
+
+  // run_c_loop (edit_engine.cpp:280-291)
+  void run_c_loop() {
+    for (;;) {
+      ++st.c_passes;
+      uint64_t pass_edits = 0;
+      for (int kind = 0; kind < 4; ++kind) pass_edits += run_subloop(kind);
+      if (pass_edits == 0) return;
+    }
+  }
+
+  uint64_t count_false_critical() {
+    reset_ctl();
+    ws.push_ctl();
+    k_detect_all<<<grid_for((n() + 15) / 16, 256, ws.sms, 16), 256, 0, ws.stream>>>(
+        s.fdir, s.gdir, n(), ws.ctl->counts, nullptr);
+    launched();
+    ++st.detect_sweeps;
+    ws.pull_ctl();
+    const Ctl& c = *ws.hctl;
+    return c.counts[0] + c.counts[1] + c.counts[2] + c.counts[3];
+  }
+
+  // run_r_loop (edit_engine.cpp:329-366).  Returns true when it stopped on
+  // matching labels (the outer loop's postcondition), false on new false CPs.
+  bool run_r_loop() {
+    uint64_t iters = 0;
+    for (;;) {
+      if (count_false_critical() != 0) return false;
+      labels_from_codes(s.gdir, lab(2), lab(3));
+      reset_ctl();
+      ws.push_ctl();
+      const uint32_t batch = ws.next_batch++;
+      k_rfix<T><<<grid_for(n(), 256, ws.sms, 16), 256, 0, ws.stream>>>(s, batch);
+      launched();
+      ws.pull_ctl();
+      const Ctl c = *ws.hctl;
+      if (c.status == kStatusTroubleMax)
+        fail(MSSZ_CU_ERR_INTERNAL, "troublemaker target is an extremum (stale critical report)");
+      if (c.mism == 0) return true;
+      if (++iters > opt.r_cap) fail(MSSZ_CU_ERR_NON_CONVERGENCE, "R-loop exceeded its iteration cap");
+      const uint32_t applied = c.s_count;
+      if (applied == 0)
+        fail(MSSZ_CU_ERR_NON_CONVERGENCE, "R-loop stalled: every troublemaker is at its floor");
+      const uint32_t mark = ws.next_mark++;
+      if (geo.ndims == 2)
+        k_frontier<T, 2><<<grid_for(applied, 256, ws.sms, 16), 256, 0, ws.stream>>>(s, applied, mark);
+      else
+        k_frontier<T, 3><<<grid_for(applied, 256, ws.sms, 16), 256, 0, ws.stream>>>(s, applied, mark);
+      launched();
+      st.effective_edits += applied;
+      ++st.r_iterations;
+      on_batch();
+    }
+  }
+
+  // Validation + EditState ctor + outer loop + tripwire (edit_engine.cpp:386-428).
+  // d_f: original (device), g already holds fhat.
+  void run(const T* d_f, double xi) {
+    if (!(xi > 0.0)) fail(MSSZ_CU_ERR_USAGE, "derive_edits requires xi > 0");
+    bind(d_f);
+    s.xi = xi;
+    reset_ctl();
+    ws.push_ctl();
+    k_validate<T><<<grid_for(n(), 256, ws.sms, 8), 256, 0, ws.stream>>>(d_f, s.g, n(), xi, ws.ctl);
+    launched();
+    ws.pull_ctl();
+    if (ws.hctl->nonfinite) fail(MSSZ_CU_ERR_IO, "derive_edits: non-finite input");
+    const uint64_t violations = ws.hctl->violations;
+    if (violations && !opt.force)
+      fail(MSSZ_CU_ERR_BOUND_VIOLATION,
+           "%llu vertices violate |f - fhat| <= xi; the preservation guarantee would not hold "
+           "(pass force to proceed anyway)",
+           (unsigned long long)violations);
+    st.input_bound_violations = violations;
+
+    // EditState ctor (edit_engine.cpp:36-56)
+    CK(cudaMemsetAsync(s.touched, 0, n(), ws.stream));
+    CK(cudaEventRecord(ws.ev[0], ws.stream));
+    directions(d_f, ws.fdir.as<uint8_t>());
+    directions(s.g, s.gdir);
+    CK(cudaEventRecord(ws.ev[1], ws.stream));
+    labels_from_codes(s.fdir, lab(0), lab(1));
+    {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, ws.ev[0], ws.ev[1]));
+      dir_ms += ms;
+    }
+
+    bool labels_verified = false;
+    for (uint64_t outer = 0;; ++outer) {
+      if (outer >= opt.outer_cap)
+        fail(MSSZ_CU_ERR_NON_CONVERGENCE,
+             "outer loop cap reached after %llu edits (%llu C sub-iterations, %llu R iterations)",
+             (unsigned long long)st.effective_edits,
+             (unsigned long long)(st.sub_iterations[0] + st.sub_iterations[1] +
+                                  st.sub_iterations[2] + st.sub_iterations[3]),
+             (unsigned long long)st.r_iterations);
+      ++st.outer_iterations;
+      const uint64_t before = st.effective_edits;
+      run_c_loop();
+      const uint64_t after_c = st.effective_edits;
+      labels_verified = run_r_loop();
+      // zero-edit R pass that ended on matching labels == the tripwire's state
+      labels_verified = labels_verified && st.effective_edits == after_c;
+      if (st.effective_edits == before) break;
+    }
+    // postcondition tripwire (edit_engine.cpp:423-428).  When the final outer
+    // pass made no edits, its R-loop already evaluated exactly this state
+    // (zero false critical points, zero mismatches); recompute otherwise.
+    if (!labels_verified) {
+      if (count_false_critical() != 0)
+        fail(MSSZ_CU_ERR_INTERNAL, "converged with false critical points");
+      labels_from_codes(s.gdir, lab(2), lab(3));
+      reset_ctl();
+      ws.push_ctl();
+      k_rfix<T><<<grid_for(n(), 256, ws.sms, 16), 256, 0, ws.stream>>>(s, ws.next_batch++);
+      launched();
+      ws.pull_ctl();
+      if (ws.hctl->mism != 0) fail(MSSZ_CU_ERR_INTERNAL, "converged with mismatched labels");
+    }
+  }
+
+  // edits() (edit_engine.cpp:368-378) into device buffers; returns the count.
+  uint64_t compact(const uint8_t* flag, uint8_t want, const T* vals, uint64_t* d_idx, T* d_val) {
+    const uint64_t ntiles = (static_cast<uint64_t>(n()) + kCompactTile - 1) / kCompactTile;
+    uint32_t* tiles = ws.tiles.as<uint32_t>();
+    k_compact_count<<<static_cast<uint32_t>(ntiles), kCompactThreads, 0, ws.stream>>>(flag, n(), want, tiles);
+    launched();
+    k_scan_tiles<<<1, 1024, 0, ws.stream>>>(tiles, ntiles, &ws.ctl->mism);
+    launched();
+    k_compact_write<T><<<static_cast<uint32_t>(ntiles), kCompactThreads, 0, ws.stream>>>(
+        flag, n(), want, vals, tiles, d_idx, d_val);
+    launched();
+    uint64_t total = 0;
+    CK(cudaMemcpyAsync(&total, &ws.ctl->mism, sizeof total, cudaMemcpyDeviceToHost, ws.stream));
+    ws.sync();
+    return total;
+  }
+
+  // device EditSet buffers inside the (now idle) worklist block
+  uint64_t* edit_idx() const { return reinterpret_cast<uint64_t*>(ws.lists.p); }
+  T* edit_val() const {
+    return reinterpret_cast<T*>(static_cast<char*>(ws.lists.p) +
+                                static_cast<uint64_t>((n() + 63) & ~63u) * 8);
+  }
+
+  void finish_stats() {
+    st.direction_seconds = dir_ms * 1e-3;
+    st.label_seconds = lab_ms * 1e-3;
+  }
+};
+
+mssz_cu_options resolve(const mssz_cu_options* o) {
+  mssz_cu_options d;
+  mssz_cu_default_options(&d);
+  return o ? *o : d;
+}
+
+double elapsed_s(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, a, b));
+  return ms * 1e-3;
+}
+
+// Host-buffer entry shared by derive_edits / derive_edits_into.
+template <class T>
+void derive_host(int ndims, const uint64_t* dims, const T* f, const T* fh, double xi,
+                 const mssz_cu_options* o, uint64_t** idx_alloc, T** val_alloc, uint64_t* idx_buf,
+                 T* val_buf, uint64_t capacity, uint64_t* count_out, mssz_cu_stats* stats_out) {
+  const Geom geo = make_geom(ndims, dims);
+  if (!f || !fh || !count_out) fail(MSSZ_CU_ERR_USAGE, "null input/output pointer");
+  const mssz_cu_options opt = resolve(o);
+  Workspace& ws = workspace(opt.device);
+  std::lock_guard<std::mutex> lk(ws.mu);
+  ws.ensure(geo.n, sizeof(T));
+  Engine<T> eng(ws, geo, opt);
+  cudaEvent_t t0, t1, t2, t3;
+  CK(cudaEventCreate(&t0));
+  CK(cudaEventCreate(&t1));
+  CK(cudaEventCreate(&t2));
+  CK(cudaEventCreate(&t3));
+  struct EvGuard {
+    cudaEvent_t* e;
+    ~EvGuard() {
+      for (int i = 0; i < 4; ++i) cudaEventDestroy(e[i]);
+    }
+  };
+  cudaEvent_t evs[4] = {t0, t1, t2, t3};
+  EvGuard guard{evs};
+  CK(cudaEventRecord(t0, ws.stream));
+  CK(cudaMemcpyAsync(ws.f.p, f, sizeof(T) * geo.n, cudaMemcpyHostToDevice, ws.stream));
+  CK(cudaMemcpyAsync(ws.g.p, fh, sizeof(T) * geo.n, cudaMemcpyHostToDevice, ws.stream));
+  CK(cudaEventRecord(t1, ws.stream));
+  eng.run(ws.f.as<T>(), xi);
+  const uint64_t count = eng.compact(eng.s.touched, 1, eng.s.g, eng.edit_idx(), eng.edit_val());
+  CK(cudaEventRecord(t2, ws.stream));
+  uint64_t* hi = idx_buf;
+  T* hv = val_buf;
+  if (idx_alloc) {
+    hi = static_cast<uint64_t*>(std::malloc(sizeof(uint64_t) * (count ? count : 1)));
+    hv = static_cast<T*>(std::malloc(sizeof(T) * (count ? count : 1)));
+    if (!hi || !hv) {
+      std::free(hi);
+      std::free(hv);
+      throw std::bad_alloc();
+    }
+  } else if (count > capacity) {
+    *count_out = count;
+    fail(MSSZ_CU_ERR_USAGE, "output capacity %llu < %llu edits", (unsigned long long)capacity,
+         (unsigned long long)count);
+  }
+  if (count) {
+    CK(cudaMemcpyAsync(hi, eng.edit_idx(), sizeof(uint64_t) * count, cudaMemcpyDeviceToHost, ws.stream));
+    CK(cudaMemcpyAsync(hv, eng.edit_val(), sizeof(T) * count, cudaMemcpyDeviceToHost, ws.stream));
+  }
+  CK(cudaEventRecord(t3, ws.stream));
+  ws.sync();
+  eng.st.touched = count;
+  eng.finish_stats();
+  eng.st.h2d_seconds = elapsed_s(t0, t1);
+  eng.st.device_seconds = elapsed_s(t1, t2);
+  eng.st.d2h_seconds = elapsed_s(t2, t3);
+  if (idx_alloc) {
+    *idx_alloc = hi;
+    *val_alloc = hv;
+  }
+  *count_out = count;
+  if (stats_out) *stats_out = eng.st;
+}
+
+template <class T>
+void derive_device(int ndims, const uint64_t* dims, const T* d_f, const T* d_fh, double xi,
+                   const mssz_cu_options* o, uint64_t* d_idx, T* d_val, uint64_t capacity,
+                   uint64_t* count_out, mssz_cu_stats* stats_out, void* stream) {
+  const Geom geo = make_geom(ndims, dims);
+  if (!d_f || !d_fh || !count_out) fail(MSSZ_CU_ERR_USAGE, "null input/output pointer");
+  const mssz_cu_options opt = resolve(o);
+  Workspace& ws = workspace(opt.device);
+  std::lock_guard<std::mutex> lk(ws.mu);
+  ws.ensure(geo.n, sizeof(T));
+  cudaStream_t caller = static_cast<cudaStream_t>(stream);
+  if (caller) {
+    CK(cudaEventRecord(ws.ev[0], caller));
+    CK(cudaStreamWaitEvent(ws.stream, ws.ev[0], 0));
+  }
+  Engine<T> eng(ws, geo, opt);
+  cudaEvent_t t0, t1;
+  CK(cudaEventCreate(&t0));
+  CK(cudaEventCreate(&t1));
+  CK(cudaEventRecord(t0, ws.stream));
+  CK(cudaMemcpyAsync(ws.g.p, d_fh, sizeof(T) * geo.n, cudaMemcpyDeviceToDevice, ws.stream));
+  eng.run(d_f, xi);
+  const uint64_t count = eng.compact(eng.s.touched, 1, eng.s.g, eng.edit_idx(), eng.edit_val());
+  if (count > capacity) {
+    *count_out = count;
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    fail(MSSZ_CU_ERR_USAGE, "output capacity %llu < %llu edits", (unsigned long long)capacity,
+         (unsigned long long)count);
+  }
+  if (count) {
+    CK(cudaMemcpyAsync(d_idx, eng.edit_idx(), sizeof(uint64_t) * count, cudaMemcpyDeviceToDevice, ws.stream));
+    CK(cudaMemcpyAsync(d_val, eng.edit_val(), sizeof(T) * count, cudaMemcpyDeviceToDevice, ws.stream));
+  }
+  CK(cudaEventRecord(t1, ws.stream));
+  ws.sync();
+  eng.st.device_seconds = elapsed_s(t0, t1);
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  if (caller) {
+    CK(cudaEventRecord(ws.ev[1], ws.stream));
+    CK(cudaStreamWaitEvent(caller, ws.ev[1], 0));
+  }
+  eng.st.touched = count;
+  eng.finish_stats();
+  *count_out = count;
+  if (stats_out) *stats_out = eng.st;
+}
+
+// ---- stand-alone kernel exports (parity harness) ----
+
+template <class T>
+struct Scratch {  // host-in/host-out helper for the per-kernel exports
+  Workspace& ws;
+  Geom geo;
+  Scratch(Workspace& w, const Geom& g) : ws(w), geo(g) {}
+};
+
+template <class T>
+void compute_dirs_host(int ndims, const uint64_t* dims, const T* values, uint8_t* codes,
+                       uint64_t* asc, uint64_t* desc) {
+  const Geom geo = make_geom(ndims, dims);
+  if (!values) fail(MSSZ_CU_ERR_USAGE, "null values");
+  mssz_cu_options opt;
+  mssz_cu_default_options(&opt);
+  Workspace& ws = workspace(-1);
+  std::lock_guard<std::mutex> lk(ws.mu);
+  ws.ensure(geo.n, sizeof(T));
+  Engine<T> eng(ws, geo, opt);
+  CK(cudaMemcpyAsync(ws.g.p, values, sizeof(T) * geo.n, cudaMemcpyHostToDevice, ws.stream));
+  eng.directions(ws.g.as<T>(), ws.gdir.as<uint8_t>());
+  if (codes)
+    CK(cudaMemcpyAsync(codes, ws.gdir.p, geo.n, cudaMemcpyDeviceToHost, ws.stream));
+  if (asc && desc) {
+    uint64_t* da = reinterpret_cast<uint64_t*>(ws.lists.p);
+    uint64_t* dd = da + ((geo.n + 63) & ~63u);
+    k_codes_to_ids<<<grid_for(geo.n, 256, ws.sms, 16), 256, 0, ws.stream>>>(ws.gdir.as<uint8_t>(), geo, da, dd);
+    CK_LAUNCH();
+    CK(cudaMemcpyAsync(asc, da, 8ull * geo.n, cudaMemcpyDeviceToHost, ws.stream));
+    CK(cudaMemcpyAsync(desc, dd, 8ull * geo.n, cudaMemcpyDeviceToHost, ws.stream));
+  }
+  ws.sync();
+}
+
+template <class T>
+__global__ void k_kind_flags(const uint8_t* __restrict__ fdir, const uint8_t* __restrict__ gdir,
+                             uint32_t n, int kind, uint8_t* __restrict__ out) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t v = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride)
+    out[v] = kind_match(kind, fdir[v], gdir[v]) ? 1 : 0;
+}
+
+template <class T>
+void detect_host(int ndims, const uint64_t* dims, const T* f, const T* g, int kind,
+                 uint64_t* counts, uint64_t* lists, uint64_t* count_out) {
+  const Geom geo = make_geom(ndims, dims);
+  if (!f || !g) fail(MSSZ_CU_ERR_USAGE, "null input");
+  if (kind > 3) fail(MSSZ_CU_ERR_USAGE, "kind must be 0..3");
+  mssz_cu_options opt;
+  mssz_cu_default_options(&opt);
+  Workspace& ws = workspace(-1);
+  std::lock_guard<std::mutex> lk(ws.mu);
+  ws.ensure(geo.n, sizeof(T));
+  Engine<T> eng(ws, geo, opt);
+  eng.bind(ws.f.as<T>());
+  CK(cudaMemcpyAsync(ws.f.p, f, sizeof(T) * geo.n, cudaMemcpyHostToDevice, ws.stream));
+  CK(cudaMemcpyAsync(ws.g.p, g, sizeof(T) * geo.n, cudaMemcpyHostToDevice, ws.stream));
+  eng.directions(ws.f.as<T>(), ws.fdir.as<uint8_t>());
+  eng.directions(ws.g.as<T>(), ws.gdir.as<uint8_t>());
+  uint8_t* cls = ws.touched.as<uint8_t>();
+  uint64_t* d_idx = eng.edit_idx();
+  if (kind < 0) {
+    eng.reset_ctl();
+    ws.push_ctl();
+    k_detect_all<<<grid_for((geo.n + 15) / 16, 256, ws.sms, 16), 256, 0, ws.stream>>>(
+        ws.fdir.as<uint8_t>(), ws.gdir.as<uint8_t>(), geo.n, ws.ctl->counts, cls);
+    CK_LAUNCH();
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t c = eng.compact(cls, static_cast<uint8_t>(k), static_cast<const T*>(nullptr), d_idx, nullptr);
+      counts[k] = c;
+      if (lists && c)
+        CK(cudaMemcpyAsync(lists + static_cast<uint64_t>(k) * geo.n, d_idx, 8 * c, cudaMemcpyDeviceToHost, ws.stream));
+      ws.sync();
+    }
+  } else {
+    k_kind_flags<T><<<grid_for(geo.n, 256, ws.sms, 16), 256, 0, ws.stream>>>(
+        ws.fdir.as<uint8_t>(), ws.gdir.as<uint8_t>(), geo.n, kind, cls);
+    CK_LAUNCH();
+    const uint64_t c = eng.compact(cls, 1, static_cast<const T*>(nullptr), d_idx, nullptr);
+    if (c) CK(cudaMemcpyAsync(lists, d_idx, 8 * c, cudaMemcpyDeviceToHost, ws.stream));
+    ws.sync();
+    *count_out = c;
+  }
+}
+
+template <class T>
+void elementwise_host(uint64_t n, const T* g, const T* f, double xi, T* out, uint8_t* moved,
+                      bool floor_only) {
+  if (n == 0) return;
+  if (!f || !out) fail(MSSZ_CU_ERR_USAGE, "null pointer");
+  Workspace& ws = workspace(-1);
+  std::lock_guard<std::mutex> lk(ws.mu);
+  DevBuf a, b, c, d;
+  struct Rel {
+    DevBuf* x[4];
+    ~Rel() {
+      for (auto* p : x) p->release();
+    }
+  } rel{{&a, &b, &c, &d}};
+  a.ensure(sizeof(T) * n);
+  b.ensure(sizeof(T) * n);
+  c.ensure(sizeof(T) * n);
+  d.ensure(n);
+  CK(cudaMemcpyAsync(b.p, f, sizeof(T) * n, cudaMemcpyHostToDevice, ws.stream));
+  const uint32_t blocks = grid_for(n, 256, ws.sms, 16);
+  if (floor_only) {
+    k_floor<T><<<blocks, 256, 0, ws.stream>>>(n, b.as<T>(), xi, c.as<T>());
+  } else {
+    CK(cudaMemcpyAsync(a.p, g, sizeof(T) * n, cudaMemcpyHostToDevice, ws.stream));
+    k_lower_step<T><<<blocks, 256, 0, ws.stream>>>(n, a.as<T>(), b.as<T>(), xi, c.as<T>(), d.as<uint8_t>());
+  }
+  CK_LAUNCH();
+  CK(cudaMemcpyAsync(out, c.p, sizeof(T) * n, cudaMemcpyDeviceToHost, ws.stream));
+  if (moved && !floor_only) CK(cudaMemcpyAsync(moved, d.p, n, cudaMemcpyDeviceToHost, ws.stream));
+  ws.sync();
+}
+
+// apply_edits (edit_engine.cpp:437-450)
+template <class T>
+void apply_host(uint64_t n, const T* fh, const uint64_t* idx, const T* vals, uint64_t count, T* out) {
+  if (!fh || !out || (count && (!idx || !vals))) fail(MSSZ_CU_ERR_USAGE, "null pointer");
+  Workspace& ws = workspace(-1);
+  std::lock_guard<std::mutex> lk(ws.mu);
+  DevBuf a, b, c, d;
+  struct Rel {
+    DevBuf* x[4];
+    ~Rel() {
+      for (auto* p : x) p->release();
+    }
+  } rel{{&a, &b, &c, &d}};
+  a.ensure(sizeof(T) * (n ? n : 1));
+  b.ensure(8 * (count ? count : 1));
+  c.ensure(sizeof(T) * (count ? count : 1));
+  d.ensure(4);
+  CK(cudaMemsetAsync(d.p, 0, 4, ws.stream));
+  CK(cudaMemcpyAsync(a.p, fh, sizeof(T) * n, cudaMemcpyHostToDevice, ws.stream));
+  if (count) {
+    CK(cudaMemcpyAsync(b.p, idx, 8 * count, cudaMemcpyHostToDevice, ws.stream));
+    CK(cudaMemcpyAsync(c.p, vals, sizeof(T) * count, cudaMemcpyHostToDevice, ws.stream));
+    k_scatter<T><<<grid_for(count, 256, ws.sms, 16), 256, 0, ws.stream>>>(count, b.as<uint64_t>(), c.as<T>(), n, a.as<T>(), d.as<uint32_t>());
+    CK_LAUNCH();
+  }
+  uint32_t bad = 0;
+  CK(cudaMemcpyAsync(&bad, d.p, 4, cudaMemcpyDeviceToHost, ws.stream));
+  CK(cudaMemcpyAsync(out, a.p, sizeof(T) * n, cudaMemcpyDeviceToHost, ws.stream));
+  ws.sync();
+  if (bad) fail(MSSZ_CU_ERR_CORRUPT_ARCHIVE, "edit index out of range");
+}
+
+void labels_host(int ndims, const uint64_t* dims, const uint64_t* asc, const uint64_t* desc,
+                 uint64_t* M, uint64_t* m) {
+  const Geom geo = make_geom(ndims, dims);
+  if (!asc || !desc || !M || !m) fail(MSSZ_CU_ERR_USAGE, "null pointer");
+  mssz_cu_options opt;
+  mssz_cu_default_options(&opt);
+  Workspace& ws = workspace(-1);
+  std::lock_guard<std::mutex> lk(ws.mu);
+  ws.ensure(geo.n, 4);
+  Engine<float> eng(ws, geo, opt);
+  const uint64_t np = (geo.n + 63) & ~63u;
+  uint64_t* da = reinterpret_cast<uint64_t*>(ws.lists.p);
+  uint64_t* dd = da + np;
+  uint32_t* LM = eng.lab(0);
+  uint32_t* Lm = eng.lab(1);
+  CK(cudaMemcpyAsync(da, asc, 8ull * geo.n, cudaMemcpyHostToDevice, ws.stream));
+  CK(cudaMemcpyAsync(dd, desc, 8ull * geo.n, cudaMemcpyHostToDevice, ws.stream));
+  eng.reset_ctl();
+  ws.push_ctl();
+  const uint32_t blocks = grid_for(geo.n, 256, ws.sms, 16);
+  k_u64_to_u32<<<blocks, 256, 0, ws.stream>>>(da, LM, geo.n, &ws.ctl->status);
+  k_u64_to_u32<<<blocks, 256, 0, ws.stream>>>(dd, Lm, geo.n, &ws.ctl->status);
+  CK_LAUNCH();
+  ws.pull_ctl();
+  if (ws.hctl->status) fail(MSSZ_CU_ERR_INTERNAL, "direction field references a vertex out of range");
+  eng.jump_to_fixpoint(LM, Lm);
+  k_u32_to_u64<<<blocks, 256, 0, ws.stream>>>(LM, da, geo.n);
+  k_u32_to_u64<<<blocks, 256, 0, ws.stream>>>(Lm, dd, geo.n);
+  CK_LAUNCH();
+  CK(cudaMemcpyAsync(M, da, 8ull * geo.n, cudaMemcpyDeviceToHost, ws.stream));
+  CK(cudaMemcpyAsync(m, dd, 8ull * geo.n, cudaMemcpyDeviceToHost, ws.stream));
+  ws.sync();
+}
+
+void classify_host(uint64_t n, const uint64_t* asc, const uint64_t* desc, uint64_t* maxima,
+                   uint64_t* nmax, uint64_t* minima, uint64_t* nmin) {
+  if (n == 0 || n >= 0xFFFFFFFFull) fail(MSSZ_CU_ERR_USAGE, "bad vertex count");
+  const uint64_t dims[2] = {n, 1};
+  Geom geo{};
+  geo.ndims = 2;
+  geo.X = static_cast<uint32_t>(n);
+  geo.Y = 1;
+  geo.Z = 1;
+  geo.XY = geo.X;
+  geo.n = static_cast<uint32_t>(n);
+  (void)dims;
+  mssz_cu_options opt;
+  mssz_cu_default_options(&opt);
+  Workspace& ws = workspace(-1);
+  std::lock_guard<std::mutex> lk(ws.mu);
+  ws.ensure(geo.n, 4);
+  Engine<float> eng(ws, geo, opt);
+  const uint64_t np = (n + 63) & ~uint64_t(63);
+  uint64_t* da = reinterpret_cast<uint64_t*>(ws.lists.p);
+  uint64_t* dd = da + np;
+  CK(cudaMemcpyAsync(da, asc, 8ull * n, cudaMemcpyHostToDevice, ws.stream));
+  CK(cudaMemcpyAsync(dd, desc, 8ull * n, cudaMemcpyHostToDevice, ws.stream));
+  k_extremum_flags<<<grid_for(n, 256, ws.sms, 16), 256, 0, ws.stream>>>(da, dd, n, ws.fdir.as<uint8_t>(), ws.gdir.as<uint8_t>());
+  CK_LAUNCH();
+  uint64_t* out = reinterpret_cast<uint64_t*>(ws.lab.p);
+  *nmax = eng.compact(ws.fdir.as<uint8_t>(), 1, static_cast<const float*>(nullptr), out, nullptr);
+  if (*nmax) CK(cudaMemcpyAsync(maxima, out, 8 * *nmax, cudaMemcpyDeviceToHost, ws.stream));
+  ws.sync();
+  *nmin = eng.compact(ws.gdir.as<uint8_t>(), 1, static_cast<const float*>(nullptr), out, nullptr);
+  if (*nmin) CK(cudaMemcpyAsync(minima, out, 8 * *nmin, cudaMemcpyDeviceToHost, ws.stream));
+  ws.sync();
+}
+
+}  // namespace
+}  // namespace mssz_b200
+
+using namespace mssz_b200;
+
+extern "C" {
+
+void mssz_cu_default_options(mssz_cu_options* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof *o);
+  o->outer_cap = 1000;
+  o->subloop_cap = 640;
+  o->r_cap = 100000;
+  o->force = 0;
+  o->device = -1;
+}
+
+const char* mssz_cu_last_error(void) { return g_last_error.c_str(); }
+void mssz_cu_free(void* p) { std::free(p); }
+const char* mssz_cu_version(void) { return "mssz-b200 0.1 (sm_100a)"; }
+
+int mssz_cu_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int mssz_cu_release_workspace(int device) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    if (device < 0) CK(cudaGetDevice(&device));
+    if (device < static_cast<int>(g_ws.size()) && g_ws[device]) {
+      std::lock_guard<std::mutex> lk2(g_ws[device]->mu);
+      g_ws[device]->release();
+    }
+  });
+}
+
+#define MSSZ_CU_DEFINE_TYPED(SUF, T)                                                              \
+  int mssz_cu_derive_edits_##SUF(int ndims, const uint64_t* dims, const T* f, const T* fh,        \
+                                 double xi, const mssz_cu_options* opt, uint64_t** idx, T** val,  \
+                                 uint64_t* count, mssz_cu_stats* st) {                            \
+    return guarded([&] {                                                                          \
+      if (!idx || !val) fail(MSSZ_CU_ERR_USAGE, "null output pointer");                          \
+      derive_host<T>(ndims, dims, f, fh, xi, opt, idx, val, nullptr, nullptr, 0, count, st);     \
+    });                                                                                           \
+  }                                                                                               \
+  int mssz_cu_derive_edits_into_##SUF(int ndims, const uint64_t* dims, const T* f, const T* fh,   \
+                                      double xi, const mssz_cu_options* opt, uint64_t* idx,       \
+                                      T* val, uint64_t cap, uint64_t* count, mssz_cu_stats* st) { \
+    return guarded([&] {                                                                          \
+      derive_host<T>(ndims, dims, f, fh, xi, opt, nullptr, nullptr, idx, val, cap, count, st);   \
+    });                                                                                           \
+  }                                                                                               \
+  int mssz_cu_derive_edits_device_##SUF(int ndims, const uint64_t* dims, const T* f,              \
+                                        const T* fh, double xi, const mssz_cu_options* opt,       \
+                                        uint64_t* idx, T* val, uint64_t cap, uint64_t* count,     \
+                                        mssz_cu_stats* st, void* stream) {                        \
+    return guarded([&] {                                                                          \
+      derive_device<T>(ndims, dims, f, fh, xi, opt, idx, val, cap, count, st, stream);           \
+    });                                                                                           \
+  }                                                                                               \
+  int mssz_cu_compute_directions_##SUF(int ndims, const uint64_t* dims, const T* v,              \
+                                       uint64_t* asc, uint64_t* desc) {                           \
+    return guarded([&] {                                                                          \
+      if (!asc || !desc) fail(MSSZ_CU_ERR_USAGE, "null output pointer");                         \
+      compute_dirs_host<T>(ndims, dims, v, nullptr, asc, desc);                                   \
+    });                                                                                           \
+  }                                                                                               \
+  int mssz_cu_compute_direction_codes_##SUF(int ndims, const uint64_t* dims, const T* v,         \
+                                            uint8_t* codes) {                                     \
+    return guarded([&] {                                                                          \
+      if (!codes) fail(MSSZ_CU_ERR_USAGE, "null output pointer");                                \
+      compute_dirs_host<T>(ndims, dims, v, codes, nullptr, nullptr);                              \
+    });                                                                                           \
+  }                                                                                               \
+  int mssz_cu_detect_false_critical_##SUF(int ndims, const uint64_t* dims, const T* f,           \
+                                          const T* g, uint64_t counts[4], uint64_t* lists) {      \
+    return guarded([&] {                                                                          \
+      if (!counts) fail(MSSZ_CU_ERR_USAGE, "null counts");                                       \
+      detect_host<T>(ndims, dims, f, g, -1, counts, lists, nullptr);                              \
+    });                                                                                           \
+  }                                                                                               \
+  int mssz_cu_detect_kind_##SUF(int ndims, const uint64_t* dims, const T* f, const T* g,         \
+                                int kind, uint64_t* list, uint64_t* count) {                      \
+    return guarded([&] {                                                                          \
+      if (!list || !count || kind < 0) fail(MSSZ_CU_ERR_USAGE, "bad arguments");                 \
+      detect_host<T>(ndims, dims, f, g, kind, nullptr, list, count);                              \
+    });                                                                                           \
+  }                                                                                               \
+  int mssz_cu_lower_step_##SUF(uint64_t n, const T* g, const T* f, double xi, T* out,           \
+                               uint8_t* moved) {                                                  \
+    return guarded([&] {                                                                          \
+      if (!g) fail(MSSZ_CU_ERR_USAGE, "null g");                                                 \
+      elementwise_host<T>(n, g, f, xi, out, moved, false);                                        \
+    });                                                                                           \
+  }                                                                                               \
+  int mssz_cu_representable_floor_##SUF(uint64_t n, const T* f, double xi, T* out) {            \
+    return guarded([&] { elementwise_host<T>(n, nullptr, f, xi, out, nullptr, true); });          \
+  }                                                                                               \
+  int mssz_cu_apply_edits_##SUF(uint64_t n, const T* fh, const uint64_t* idx, const T* vals,     \
+                                uint64_t count, T* out) {                                         \
+    return guarded([&] { apply_host<T>(n, fh, idx, vals, count, out); });                         \
+  }
+
+MSSZ_CU_DEFINE_TYPED(f32, float)
+MSSZ_CU_DEFINE_TYPED(f64, double)
+
+int mssz_cu_compute_labels(int ndims, const uint64_t* dims, const uint64_t* asc,
+                           const uint64_t* desc, uint64_t* M, uint64_t* m) {
+  return guarded([&] { labels_host(ndims, dims, asc, desc, M, m); });
+}
+
+int mssz_cu_classify_critical(uint64_t n, const uint64_t* asc, const uint64_t* desc,
+                              uint64_t* maxima, uint64_t* n_max, uint64_t* minima,
+                              uint64_t* n_min) {
+  return guarded([&] {
+    if (!asc || !desc || !maxima || !minima || !n_max || !n_min)
+      fail(MSSZ_CU_ERR_USAGE, "null pointer");
+    classify_host(n, asc, desc, maxima, n_max, minima, n_min);
+  });
+}
+
+}  // extern "C"
