@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 correction loop (BASELINE.json metric: Mvertices/s of
+end-to-end correction to convergence; per-kernel HBM GB/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl reference]
+
+A "step" is one full derive_edits (validation → C/R loops to convergence →
+postconditions → EditSet compaction) over one synthetic field.
+
+* value  — device-resident: f and f̂ already in HBM, EditSet left in HBM;
+           CUDA events on the caller stream around every step (L2 flushed
+           between steps by a 512 MB write outside the events); max over ranks.
+* e2e    — the public host API (derive_edits_into) from pinned host buffers:
+           H2D of f and f̂ plus D2H of the EditSet inside the timed region.
+* roofline — the dominant kernel class by device time, from per-launch CUDA
+           events on the engine's stream during the timed steps (profile=1),
+           achieved = algorithmic bytes per launch / mean launch time.
+* cpu_baseline — the UNMODIFIED reference (oracle/_ref/libmssz_ref.so,
+           OpenMP, all host cores) on a bounded sample of the same workload.
+
+N > 1 (torchrun): every rank corrects its own replica of the field (weak
+scaling; z-slab sharding of one field is the next multi-GPU step).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Mvertices/s end-to-end correction (to convergence)"
+UNIT = "Mvertices/s"
+
+# algorithmic bytes per vertex per launch (f32 values)
+def alg_bytes_per_vertex(cls: str, es: int) -> float:
+    return {
+        "validate": 2 * es,
+        "directions": es + 1,
+        "detect_kind": 2,
+        "detect_all": 2,
+        "label_init": 1 + 8,
+        "label_jump": 24,
+        "rfix": 2 + 16,
+        "compact": 2,
+    }.get(cls, 0.0)
+
+
+# bounded CPU samples (about 5-20 s of reference work on 16 host cores)
+CPU_SAMPLE = {
+    "C1": (512, 512), "C2": (177, 95, 48), "C2-trig": (177, 95, 48),
+    "C3": (96, 96, 96), "C4": (128, 128, 64), "C5": (720, 480),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--dims", default=None, help="override dims, e.g. 256x256x256")
+    ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--cpu-dims", default=None)
+    return ap.parse_args()
+
+
+def dims_arg(s):
+    return tuple(int(x) for x in s.lower().split("x")) if s else None
+
+
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+
+    def init(self, use_cuda=True):
+        if self.world > 1:
+            import torch.distributed as dist
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            backend = "nccl" if use_cuda else "gloo"
+            if use_cuda:
+                import torch
+                torch.cuda.set_device(self.local)
+            dist.init_process_group(backend)
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, x: float) -> float:
+        if not self.pg:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x: float) -> float:
+        if not self.pg:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        self.pg.all_reduce(t)
+        return float(t.item())
+
+    def done(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.fp = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.fp, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.fp.flush()
+        self.fp.seek(0)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.fp.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        os.unlink(self.fp.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fp:
+            d = json.load(fp)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_reference_run(cfg, dims, dtype, threads, steps=1):
+    """The unmodified reference derive_edits on the host (oracle/_ref): returns (times, stats)."""
+    import oracle as O
+    if not O.have_ref():
+        raise RuntimeError("oracle/_ref/libmssz_ref.so missing (build() it in the build container)")
+    R = O.ref()
+    # inputs through the reference's own generator and codec
+    if cfg.kind == "multi-scale":
+        gm = R.generate("gaussian-mixture", list(dims), cfg.seed, np.float64)
+        rs = R.generate("random-smooth", list(dims), cfg.seed + 1, np.float64)
+        f = (gm + cfg.a * rs).astype(dtype)
+    else:
+        f = R.generate(cfg.kind, list(dims), cfg.seed, dtype)
+    xi = R.resolve_rel(list(dims), f, cfg.rel)
+    fh = R.compress_base(list(dims), f, xi)
+    times, res = [], None
+    for _ in range(steps):
+        t = time.perf_counter()
+        res = R.derive_edits(list(dims), f, fh, xi, subloop_cap=cfg.subloop_cap, threads=threads)
+        times.append(time.perf_counter() - t)
+    return times, res.stats
+
+
+def run_reference_arm(args, cfg, dist):
+    if dist.rank != 0:
+        return
+    dims = dims_arg(args.cpu_dims) or CPU_SAMPLE.get(cfg.name, cfg.dims)
+    dtype = np.float32 if args.dtype == "f32" else np.float64
+    threads = os.cpu_count() or 1
+    os.environ.setdefault("OMP_WAIT_POLICY", "active")
+    times, st = cpu_reference_run(cfg, dims, dtype, threads, steps=args.warmup + args.steps)
+    timed = times[args.warmup:]
+    n = int(np.prod(dims))
+    mean = statistics.mean(timed)
+    value = n / mean / 1e6
+    sample = f"{cfg.name} kind={cfg.kind} at {'x'.join(map(str, dims))} ({n} vertices), rel {cfg.rel}"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": mean * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+        "config": {"workload": cfg.note, "sample_dims": list(dims), "rel_eb": cfg.rel,
+                   "subloop_cap": cfg.subloop_cap, "parallelism": "openmp"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "edit_stats": st,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    from paper_2406_09423_b200 import inputs as I
+    cfg = I.CONFIGS[args.config]
+    dist = Dist()
+    if args.impl == "reference":
+        run_reference_arm(args, cfg, dist)
+        return
+
+    import torch
+    import paper_2406_09423_b200 as P
+
+    dist.init()
+    torch.cuda.set_device(dist.local)
+    dtype = np.float32 if args.dtype == "f32" else np.float64
+    tdtype = torch.float32 if args.dtype == "f32" else torch.float64
+    es = 4 if args.dtype == "f32" else 8
+    dims = dims_arg(args.dims) or cfg.dims
+    topo = P.build_topology(dims)
+    n = topo.vertex_count
+
+    t_gen = time.perf_counter()
+    f, fh, xi = I.make_inputs(cfg, dims, dtype)
+    t_gen = time.perf_counter() - t_gen
+
+    dev = torch.device("cuda", dist.local)
+    df = torch.from_numpy(f).to(dev)
+    dfh = torch.from_numpy(fh).to(dev)
+    cap = n
+    d_idx = torch.empty(cap, dtype=torch.int64, device=dev)
+    d_val = torch.empty(cap, dtype=tdtype, device=dev)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    opts = P.DeriveOptions(subloop_cap=cfg.subloop_cap, device=dist.local,
+                           profile=not args.no_profile)
+
+    def step():
+        return P.derive_edits_device(topo, df.data_ptr(), dfh.data_ptr(), xi, d_idx.data_ptr(),
+                                     d_val.data_ptr(), cap, dtype, opts, stream.cuda_stream)
+
+    for _ in range(args.warmup):
+        count, st = step()
+    torch.cuda.synchronize()
+
+    dist.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(dist.local)
+    step_ms, stats = [], []
+    for _ in range(args.steps):
+        flush.fill_(1.0)  # evict L2 between steps (outside the events)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        count, st = step()
+        b.record(stream)
+        b.synchronize()
+        step_ms.append(a.elapsed_time(b))
+        stats.append(st)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk = clocks.stop()
+    ms = dist.max(statistics.mean(step_ms))
+    total_vertices = dist.sum(float(n))
+    value = total_vertices / (ms * 1e-3) / 1e6
+
+    # ---- roofline of the dominant kernel class (live, from the timed steps)
+    peak, peak_src = load_peaks()
+    roofline = None
+    prof = {}
+    if not args.no_profile:
+        agg = {name: {"launches": 0, "ms": 0.0} for name in P.PROF_CLASSES}
+        for s in stats:
+            for name, d in s.kernel_profile().items():
+                agg[name]["launches"] += d["launches"]
+                agg[name]["ms"] += d["ms"]
+        prof = {k: {"launches": v["launches"] // len(stats), "ms": v["ms"] / len(stats)}
+                for k, v in agg.items() if v["launches"]}
+        graded = {k: v for k, v in agg.items() if alg_bytes_per_vertex(k, es) and v["launches"]}
+        top = max(graded, key=lambda k: graded[k]["ms"])
+        per_launch_ms = graded[top]["ms"] / graded[top]["launches"]
+        bytes_per_launch = alg_bytes_per_vertex(top, es) * n
+        achieved = bytes_per_launch / (per_launch_ms * 1e-3) / 1e9
+        total_ms = sum(v["ms"] for v in agg.values())
+        roofline = {"kernel": top, "bound": "hbm", "achieved": achieved, "peak": peak,
+                    "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                    "peak_source": peak_src,
+                    "alg_bytes_per_launch": bytes_per_launch,
+                    "mean_launch_us": per_launch_ms * 1e3,
+                    "share_of_device_time": graded[top]["ms"] / total_ms if total_ms else None}
+
+    # ---- e2e through the host API with pinned buffers
+    e2e = None
+    if not args.no_e2e:
+        hf = torch.from_numpy(f).pin_memory()
+        hfh = torch.from_numpy(fh).pin_memory()
+        h_idx = torch.empty(max(count, 1), dtype=torch.int64).pin_memory()
+        h_val = torch.empty(max(count, 1), dtype=tdtype).pin_memory()
+        e2e_opts = P.DeriveOptions(subloop_cap=cfg.subloop_cap, device=dist.local)
+        P.derive_edits_into(topo, hf.data_ptr(), hfh.data_ptr(), xi, h_idx.data_ptr(),
+                            h_val.data_ptr(), h_idx.numel(), dtype, e2e_opts)
+        walls = []
+        dist.barrier()
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            c2, _ = P.derive_edits_into(topo, hf.data_ptr(), hfh.data_ptr(), xi, h_idx.data_ptr(),
+                                        h_val.data_ptr(), h_idx.numel(), dtype, e2e_opts)
+            walls.append(time.perf_counter() - t)
+        wall = dist.max(statistics.mean(walls))
+        e2e = {"value": total_vertices / wall / 1e6, "unit": UNIT,
+               "h2d_bytes_per_step": 2 * n * es, "d2h_bytes_per_step": int(c2) * (8 + es),
+               "ms_per_step": wall * 1e3, "api": "mssz_cu_derive_edits_into (pinned host buffers)"}
+
+    # ---- CPU baseline: the unmodified reference on a bounded sample (rank 0, N=1)
+    cpu = None
+    if not args.no_cpu and dist.rank == 0 and dist.world == 1:
+        sdims = dims_arg(args.cpu_dims) or CPU_SAMPLE.get(cfg.name, cfg.dims)
+        threads = os.cpu_count() or 1
+        os.environ.setdefault("OMP_WAIT_POLICY", "active")
+        try:
+            times, cst = cpu_reference_run(cfg, sdims, dtype, threads, steps=1)
+            sn = int(np.prod(sdims))
+            cpu = {"value": sn / times[0] / 1e6, "unit": UNIT, "cores": threads,
+                   "kind": "reference",
+                   "sample": f"derive_edits on {cfg.kind} {'x'.join(map(str, sdims))} "
+                             f"({sn} vertices), rel {cfg.rel}, {times[0]:.2f} s",
+                   "edit_stats": cst}
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    st = stats[-1]
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": args.dtype, "data": "synthetic",
+        "config": {"workload": cfg.note, "dims": list(dims), "vertices": n, "kind": cfg.kind,
+                   "rel_eb": cfg.rel, "xi": xi, "subloop_cap": cfg.subloop_cap,
+                   "parallelism": f"replica-per-gpu x{dist.world}",
+                   "l2": "flushed between steps (512 MB write outside the timed events)",
+                   "input_gen_s": round(t_gen, 2)},
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": int(sum(s.kernel_launches for s in stats)),
+        "clocks": clk,
+        "edit_stats": {"outer_iterations": st.outer_iterations, "c_passes": st.c_passes,
+                       "sub_iterations": st.sub_iterations, "r_iterations": st.r_iterations,
+                       "effective_edits": st.effective_edits, "touched": st.touched,
+                       "label_passes": st.label_passes, "label_rounds": st.label_rounds,
+                       "detect_sweeps": st.detect_sweeps,
+                       "frontier_vertices": st.frontier_vertices},
+        "kernel_profile_ms_per_step": prof,
+    }
+    if dist.rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.done()
+
+
+if __name__ == "__main__":
+    main()

@@ -71,7 +71,22 @@ typedef struct mssz_cu_options {
   int32_t device;       /* CUDA ordinal; -1 = current device */
   void (*on_batch)(const void* g_host, uint64_t n, void* user); /* NULL = off */
   void* on_batch_user;
+  int32_t profile; /* 1 = time every kernel with CUDA events (stats.kernel_ms) */
+  int32_t reserved;
 } mssz_cu_options;
+
+/* kernel classes of mssz_cu_stats.kernel_ms / kernel_count */
+#define MSSZ_CU_PROF_VALIDATE 0
+#define MSSZ_CU_PROF_DIRECTIONS 1
+#define MSSZ_CU_PROF_DETECT_KIND 2
+#define MSSZ_CU_PROF_DETECT_ALL 3
+#define MSSZ_CU_PROF_SUBLOOP 4
+#define MSSZ_CU_PROF_LABEL_INIT 5
+#define MSSZ_CU_PROF_LABEL_JUMP 6
+#define MSSZ_CU_PROF_RFIX 7
+#define MSSZ_CU_PROF_FRONTIER 8
+#define MSSZ_CU_PROF_COMPACT 9
+#define MSSZ_CU_PROF_CLASSES 16
 
 /* Mirrors EditStats (edit_engine.hpp:54-68) field for field, then adds the
  * device-side timings/counters of the B200 engine. */
@@ -94,6 +109,8 @@ typedef struct mssz_cu_stats {
   uint64_t detect_sweeps;
   uint64_t frontier_vertices; /* sum over batches of |S ∪ N(S)| re-evaluated */
   uint64_t kernel_launches;   /* kernels launched by this call */
+  uint64_t kernel_count[MSSZ_CU_PROF_CLASSES]; /* launches per kernel class */
+  double kernel_ms[MSSZ_CU_PROF_CLASSES];      /* device ms per class (profile = 1 only) */
 } mssz_cu_stats;
 
 void mssz_cu_default_options(mssz_cu_options* opt);

@@ -121,6 +121,7 @@ class DeriveOptions:
     force: bool = False
     device: int = -1
     on_batch: Optional[Callable[[np.ndarray], None]] = None
+    profile: bool = False  # per-kernel CUDA-event timing into EditStats.kernel_ms
 
 
 @dataclass
@@ -144,6 +145,12 @@ class EditStats:
     detect_sweeps: int = 0
     frontier_vertices: int = 0
     kernel_launches: int = 0
+    kernel_count: list = field(default_factory=lambda: [0] * 16)
+    kernel_ms: list = field(default_factory=lambda: [0.0] * 16)
+
+    def kernel_profile(self) -> dict:
+        return {name: {"launches": self.kernel_count[i], "ms": self.kernel_ms[i]}
+                for i, name in enumerate(PROF_CLASSES)}
 
     def sub_iterations_total(self) -> int:
         return sum(self.sub_iterations)
@@ -219,6 +226,7 @@ class _Options(C.Structure):
         ("outer_cap", C.c_uint64), ("subloop_cap", C.c_uint64), ("r_cap", C.c_uint64),
         ("force", C.c_int32), ("device", C.c_int32),
         ("on_batch", C.c_void_p), ("on_batch_user", C.c_void_p),
+        ("profile", C.c_int32), ("reserved", C.c_int32),
     ]
 
 
@@ -233,13 +241,19 @@ class _Stats(C.Structure):
         ("label_passes", C.c_uint64), ("label_rounds", C.c_uint64),
         ("detect_sweeps", C.c_uint64), ("frontier_vertices", C.c_uint64),
         ("kernel_launches", C.c_uint64),
+        ("kernel_count", C.c_uint64 * 16), ("kernel_ms", C.c_double * 16),
     ]
 
     def fill(self, st: EditStats) -> EditStats:
         for name, _ in self._fields_:
             v = getattr(self, name)
-            setattr(st, name, list(v) if name == "sub_iterations" else v)
+            setattr(st, name, list(v) if name in _ARRAY_FIELDS else v)
         return st
+
+
+_ARRAY_FIELDS = ("sub_iterations", "kernel_count", "kernel_ms")
+PROF_CLASSES = ["validate", "directions", "detect_kind", "detect_all", "subloop", "label_init",
+                "label_jump", "rfix", "frontier", "compact"]
 
 
 _BATCH_CB = C.CFUNCTYPE(None, C.c_void_p, C.c_uint64, C.c_void_p)
@@ -308,7 +322,8 @@ def _field(topo: GridTopology, a, name: str, dtype=None) -> np.ndarray:
 
 def _options(opts: Optional[DeriveOptions], dtype, keep: list) -> _Options:
     o = opts or DeriveOptions()
-    co = _Options(o.outer_cap, o.subloop_cap, o.r_cap, int(o.force), o.device, None, None)
+    co = _Options(o.outer_cap, o.subloop_cap, o.r_cap, int(o.force), o.device, None, None,
+                  int(o.profile), 0)
     if o.on_batch is not None:
         ctype = _ctype(dtype)
 

@@ -150,7 +150,16 @@ struct Workspace {
   Ctl* hctl = nullptr;  // pinned mirror
   uint32_t next_batch = 1, next_mark = 1;
   cudaEvent_t ev[4] = {};
+  std::vector<cudaEvent_t> pev;  // profiling event pool
   std::mutex mu;
+
+  void prof_ev(size_t need) {
+    while (pev.size() < need + 2) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      pev.push_back(e);
+    }
+  }
   uint64_t launches = 0;
 
   void init(int dev) {
@@ -220,6 +229,20 @@ Workspace& workspace(int device) {
 
 const char* kKindName[4] = {"FPmax", "FPmin", "FNmax", "FNmin"};
 
+// kernel classes of mssz_cu_stats::kernel_ms / kernel_count (MSSZ_CU_PROF_*)
+enum {
+  kProfValidate = MSSZ_CU_PROF_VALIDATE,
+  kProfDirections = MSSZ_CU_PROF_DIRECTIONS,
+  kProfDetectKind = MSSZ_CU_PROF_DETECT_KIND,
+  kProfDetectAll = MSSZ_CU_PROF_DETECT_ALL,
+  kProfSubloop = MSSZ_CU_PROF_SUBLOOP,
+  kProfLabelInit = MSSZ_CU_PROF_LABEL_INIT,
+  kProfLabelJump = MSSZ_CU_PROF_LABEL_JUMP,
+  kProfRfix = MSSZ_CU_PROF_RFIX,
+  kProfFrontier = MSSZ_CU_PROF_FRONTIER,
+  kProfCompact = MSSZ_CU_PROF_COMPACT,
+};
+
 // ---------------------------------------------------------------------------
 template <class T>
 struct Engine {
@@ -231,6 +254,8 @@ struct Engine {
   uint32_t cur = 0;
   int coop_blocks = 0;
   std::vector<T> host_g;  // on_batch snapshots only
+  size_t prof_n = 0;
+  std::vector<int> prof_cls;
   float dir_ms = 0.f, lab_ms = 0.f;
 
   Engine(Workspace& w, const Geom& g, const mssz_cu_options& o) : ws(w), geo(g), opt(o) {}
@@ -260,17 +285,41 @@ struct Engine {
     s.ctl = ws.ctl;
   }
 
-  void launched() {
+  // Per-kernel-class device time (CUDA events on the launching stream), only
+  // when opt.profile is set: bench.py's roofline reads kernel_ms / kernel_count.
+  void pre(int cls) {
+    if (!opt.profile) return;
+    ws.prof_ev(prof_n * 2);
+    CK(cudaEventRecord(ws.pev[prof_n * 2], ws.stream));
+    prof_cls.push_back(cls);
+  }
+  void launched(int cls) {
     ++ws.launches;
     ++st.kernel_launches;
+    ++st.kernel_count[cls];
     CK_LAUNCH();
+    if (!opt.profile) return;
+    CK(cudaEventRecord(ws.pev[prof_n * 2 + 1], ws.stream));
+    ++prof_n;
+  }
+  void resolve_profile() {
+    if (!opt.profile) return;
+    ws.sync();
+    for (size_t i = 0; i < prof_n; ++i) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, ws.pev[2 * i], ws.pev[2 * i + 1]));
+      st.kernel_ms[prof_cls[i]] += ms;
+    }
+    prof_n = 0;
+    prof_cls.clear();
   }
 
   void directions(const T* vals, uint8_t* dir) {
     dim3 block(128), grid((geo.X + 127) / 128, geo.Y, geo.Z);
+    pre(kProfDirections);
     if (geo.ndims == 2) k_directions<T, 2><<<grid, block, 0, ws.stream>>>(vals, dir, geo);
     else k_directions<T, 3><<<grid, block, 0, ws.stream>>>(vals, dir, geo);
-    launched();
+    launched(kProfDirections);
   }
 
   // Pointer-jumping labels; M/m already initialised (codes: k_label_init).
@@ -283,8 +332,9 @@ struct Engine {
       const int group = 4;
       CK(cudaMemsetAsync(ws.ctl->flags, 0, sizeof(uint32_t) * group, ws.stream));
       for (int r = 0; r < group; ++r) {
+        pre(kProfLabelJump);
         k_label_jump<<<blocks, 256, 0, ws.stream>>>(M, m, n(), &ws.ctl->flags[r]);
-        launched();
+        launched(kProfLabelJump);
       }
       uint32_t flags[4];
       CK(cudaMemcpyAsync(flags, ws.ctl->flags, sizeof flags, cudaMemcpyDeviceToHost, ws.stream));
@@ -302,8 +352,9 @@ struct Engine {
 
   void labels_from_codes(const uint8_t* dir, uint32_t* M, uint32_t* m) {
     CK(cudaEventRecord(ws.ev[2], ws.stream));
+    pre(kProfLabelInit);
     k_label_init<<<grid_for(n(), 256, ws.sms, 16), 256, 0, ws.stream>>>(dir, geo, M, m);
-    launched();
+    launched(kProfLabelInit);
     jump_to_fixpoint(M, m);
     CK(cudaEventRecord(ws.ev[3], ws.stream));
     CK(cudaEventSynchronize(ws.ev[3]));
@@ -342,9 +393,10 @@ struct Engine {
   uint64_t run_subloop(int kind) {
     reset_ctl();
     ws.push_ctl();
+    pre(kProfDetectKind);
     k_detect_kind<<<grid_for((n() + 15) / 16, 256, ws.sms, 16), 256, 0, ws.stream>>>(
         s.fdir, s.gdir, n(), kind, s.list[cur], &ws.ctl->list_count[cur]);
-    launched();
+    launched(kProfDetectKind);
     ++st.detect_sweeps;
     const uint32_t batch_base = ws.next_batch, mark_base = ws.next_mark;
     uint64_t cap = opt.subloop_cap;
@@ -354,8 +406,9 @@ struct Engine {
     const int blocks = coop_grid();
     uint64_t seen_iters = 0;
     for (;;) {
+      pre(kProfSubloop);
       CK(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(512), args, 0, ws.stream));
-      launched();
+      launched(kProfSubloop);
       ws.pull_ctl();
       const Ctl& c = *ws.hctl;
       if (!opt.on_batch || c.status != kStatusOk) break;
@@ -390,9 +443,10 @@ struct Engine {
   uint64_t count_false_critical() {
     reset_ctl();
     ws.push_ctl();
+    pre(kProfDetectAll);
     k_detect_all<<<grid_for((n() + 15) / 16, 256, ws.sms, 16), 256, 0, ws.stream>>>(
         s.fdir, s.gdir, n(), ws.ctl->counts, nullptr);
-    launched();
+    launched(kProfDetectAll);
     ++st.detect_sweeps;
     ws.pull_ctl();
     const Ctl& c = *ws.hctl;
@@ -409,8 +463,9 @@ struct Engine {
       reset_ctl();
       ws.push_ctl();
       const uint32_t batch = ws.next_batch++;
+      pre(kProfRfix);
       k_rfix<T><<<grid_for(n(), 256, ws.sms, 16), 256, 0, ws.stream>>>(s, batch);
-      launched();
+      launched(kProfRfix);
       ws.pull_ctl();
       const Ctl c = *ws.hctl;
       if (c.status == kStatusTroubleMax)
@@ -421,11 +476,12 @@ struct Engine {
       if (applied == 0)
         fail(MSSZ_CU_ERR_NON_CONVERGENCE, "R-loop stalled: every troublemaker is at its floor");
       const uint32_t mark = ws.next_mark++;
+      pre(kProfFrontier);
       if (geo.ndims == 2)
         k_frontier<T, 2><<<grid_for(applied, 256, ws.sms, 16), 256, 0, ws.stream>>>(s, applied, mark);
       else
         k_frontier<T, 3><<<grid_for(applied, 256, ws.sms, 16), 256, 0, ws.stream>>>(s, applied, mark);
-      launched();
+      launched(kProfFrontier);
       st.effective_edits += applied;
       ++st.r_iterations;
       on_batch();
@@ -440,8 +496,9 @@ struct Engine {
     s.xi = xi;
     reset_ctl();
     ws.push_ctl();
+    pre(kProfValidate);
     k_validate<T><<<grid_for(n(), 256, ws.sms, 8), 256, 0, ws.stream>>>(d_f, s.g, n(), xi, ws.ctl);
-    launched();
+    launched(kProfValidate);
     ws.pull_ctl();
     if (ws.hctl->nonfinite) fail(MSSZ_CU_ERR_IO, "derive_edits: non-finite input");
     const uint64_t violations = ws.hctl->violations;
@@ -492,8 +549,9 @@ struct Engine {
       labels_from_codes(s.gdir, lab(2), lab(3));
       reset_ctl();
       ws.push_ctl();
+      pre(kProfRfix);
       k_rfix<T><<<grid_for(n(), 256, ws.sms, 16), 256, 0, ws.stream>>>(s, ws.next_batch++);
-      launched();
+      launched(kProfRfix);
       ws.pull_ctl();
       if (ws.hctl->mism != 0) fail(MSSZ_CU_ERR_INTERNAL, "converged with mismatched labels");
     }
@@ -503,13 +561,16 @@ struct Engine {
   uint64_t compact(const uint8_t* flag, uint8_t want, const T* vals, uint64_t* d_idx, T* d_val) {
     const uint64_t ntiles = (static_cast<uint64_t>(n()) + kCompactTile - 1) / kCompactTile;
     uint32_t* tiles = ws.tiles.as<uint32_t>();
+    pre(kProfCompact);
     k_compact_count<<<static_cast<uint32_t>(ntiles), kCompactThreads, 0, ws.stream>>>(flag, n(), want, tiles);
-    launched();
+    launched(kProfCompact);
+    pre(kProfCompact);
     k_scan_tiles<<<1, 1024, 0, ws.stream>>>(tiles, ntiles, &ws.ctl->mism);
-    launched();
+    launched(kProfCompact);
+    pre(kProfCompact);
     k_compact_write<T><<<static_cast<uint32_t>(ntiles), kCompactThreads, 0, ws.stream>>>(
         flag, n(), want, vals, tiles, d_idx, d_val);
-    launched();
+    launched(kProfCompact);
     uint64_t total = 0;
     CK(cudaMemcpyAsync(&total, &ws.ctl->mism, sizeof total, cudaMemcpyDeviceToHost, ws.stream));
     ws.sync();
@@ -524,6 +585,7 @@ struct Engine {
   }
 
   void finish_stats() {
+    resolve_profile();
     st.direction_seconds = dir_ms * 1e-3;
     st.label_seconds = lab_ms * 1e-3;
   }
