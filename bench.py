@@ -47,8 +47,8 @@ def alg_bytes_per_vertex(cls: str, es: int) -> float:
         "directions": es + 1,
         "detect_kind": 2,
         "detect_all": 2,
-        "label_init": 1 + 8,
-        "label_jump": 24,
+        "label_init": 1 + 8,      # k_label_tile: dir byte in, two u32 labels out
+        "label_finish": 8 + 8,    # read both labels + one gather each (writes only if changed)
         "rfix": 2 + 16,
         "compact": 2,
     }.get(cls, 0.0)

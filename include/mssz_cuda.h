@@ -81,11 +81,13 @@ typedef struct mssz_cu_options {
 #define MSSZ_CU_PROF_DETECT_KIND 2
 #define MSSZ_CU_PROF_DETECT_ALL 3
 #define MSSZ_CU_PROF_SUBLOOP 4
-#define MSSZ_CU_PROF_LABEL_INIT 5
-#define MSSZ_CU_PROF_LABEL_JUMP 6
+#define MSSZ_CU_PROF_LABEL_INIT 5 /* tiled label pass (k_label_tile) */
+#define MSSZ_CU_PROF_LABEL_JUMP 6 /* pointer jumping (exits / generic API) */
 #define MSSZ_CU_PROF_RFIX 7
 #define MSSZ_CU_PROF_FRONTIER 8
 #define MSSZ_CU_PROF_COMPACT 9
+#define MSSZ_CU_PROF_LABEL_FINISH 10
+#define MSSZ_CU_PROF_FIX 11 /* host-driven huge batch: fix_list */
 #define MSSZ_CU_PROF_CLASSES 16
 
 /* Mirrors EditStats (edit_engine.hpp:54-68) field for field, then adds the
@@ -109,6 +111,8 @@ typedef struct mssz_cu_stats {
   uint64_t detect_sweeps;
   uint64_t frontier_vertices; /* sum over batches of |S ∪ N(S)| re-evaluated */
   uint64_t kernel_launches;   /* kernels launched by this call */
+  uint64_t big_batches;       /* C batches run grid-wide inside the persistent kernel */
+  uint64_t huge_batches;      /* C batches run by host-launched streaming kernels */
   uint64_t kernel_count[MSSZ_CU_PROF_CLASSES]; /* launches per kernel class */
   double kernel_ms[MSSZ_CU_PROF_CLASSES];      /* device ms per class (profile = 1 only) */
 } mssz_cu_stats;

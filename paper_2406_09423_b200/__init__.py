@@ -145,6 +145,8 @@ class EditStats:
     detect_sweeps: int = 0
     frontier_vertices: int = 0
     kernel_launches: int = 0
+    big_batches: int = 0
+    huge_batches: int = 0
     kernel_count: list = field(default_factory=lambda: [0] * 16)
     kernel_ms: list = field(default_factory=lambda: [0.0] * 16)
 
@@ -240,7 +242,8 @@ class _Stats(C.Structure):
         ("d2h_seconds", C.c_double), ("device_seconds", C.c_double),
         ("label_passes", C.c_uint64), ("label_rounds", C.c_uint64),
         ("detect_sweeps", C.c_uint64), ("frontier_vertices", C.c_uint64),
-        ("kernel_launches", C.c_uint64),
+        ("kernel_launches", C.c_uint64), ("big_batches", C.c_uint64),
+        ("huge_batches", C.c_uint64),
         ("kernel_count", C.c_uint64 * 16), ("kernel_ms", C.c_double * 16),
     ]
 
@@ -253,7 +256,7 @@ class _Stats(C.Structure):
 
 _ARRAY_FIELDS = ("sub_iterations", "kernel_count", "kernel_ms")
 PROF_CLASSES = ["validate", "directions", "detect_kind", "detect_all", "subloop", "label_init",
-                "label_jump", "rfix", "frontier", "compact"]
+                "label_jump", "rfix", "frontier", "compact", "label_finish", "fix"]
 
 
 _BATCH_CB = C.CFUNCTYPE(None, C.c_void_p, C.c_uint64, C.c_void_p)

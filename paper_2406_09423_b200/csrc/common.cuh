@@ -115,54 +115,60 @@ __device__ __forceinline__ int32_t slot_offset(const Geom& g, int k) {
   return dx + dy * static_cast<int32_t>(g.X) + dz * static_cast<int32_t>(g.XY);
 }
 
+// Index-rank order of the stencil slots (plus SELF = 15): the linear offsets
+// of grid.cpp:8-16 sort the same way for every grid with extents >= 2
+//   3D: -1-X-XY < -X-XY < -1-XY < -XY < -1-X < -X < -1 < 0 < 1 < X < 1+X < XY
+//       < 1+XY < X+XY < 1+X+XY
+//   2D: -1-X < -X < -1 < 0 < 1 < X < 1+X
+// so SoS (value, then index) reduces to comparing keys while scanning slots in
+// this order: ascending uses >= (the highest index wins a tie), descending
+// uses < (the lowest index wins), exactly sos_greater / sos_less (grid.hpp:53-63).
+template <int DIM>
+__host__ __device__ __forceinline__ constexpr int rank_slot(int r) {
+  if (DIM == 2) {
+    constexpr int t[7] = {5, 3, 1, 15, 0, 2, 4};
+    return t[r];
+  } else {
+    constexpr int t[15] = {13, 9, 11, 5, 7, 3, 1, 15, 0, 2, 6, 4, 10, 8, 12};
+    return t[r];
+  }
+}
+
 // Steepest ascending / descending slot of v over self ∪ link (mss.cpp:11-30):
 // returns (asc | desc << 4), SELF = 15.
 template <class T, int DIM, bool kCoherent>
 __device__ __forceinline__ uint32_t direction_code(const T* __restrict__ vals, const Geom& g,
                                                    uint32_t v, uint32_t x, uint32_t y,
                                                    uint32_t z) {
-  constexpr int NS = StencilSize<DIM>::value;
-  if constexpr (sizeof(T) == 4) {
-    const uint64_t kv = (static_cast<uint64_t>(okey(ld<kCoherent>(vals + v))) << 32) | v;
-    uint64_t hi = kv, lo = kv;
-    uint32_t hc = kSelf, lc = kSelf;
+  using K = typename KeyOf<T>::type;
+  constexpr int NR = StencilSize<DIM>::value + 1;
+  const bool interior = x > 0 && x + 1 < g.X && y > 0 && y + 1 < g.Y &&
+                        (DIM == 2 || (z > 0 && z + 1 < g.Z));
+  // all loads first (out-of-grid slots re-read v and are masked below)
+  K key[NR];
+  bool ok[NR];
 #pragma unroll
-    for (int k = 0; k < NS; ++k) {
-      if (!in_grid<DIM>(g, x, y, z, k)) continue;
-      const uint32_t u = v + slot_offset<DIM>(g, k);
-      const uint64_t ku = (static_cast<uint64_t>(okey(ld<kCoherent>(vals + u))) << 32) | u;
-      if (ku > hi) {
-        hi = ku;
-        hc = k;
-      }
-      if (ku < lo) {
-        lo = ku;
-        lc = k;
-      }
-    }
-    return hc | (lc << 4);
-  } else {
-    const uint64_t kv = okey(ld<kCoherent>(vals + v));
-    uint64_t hk = kv, lk = kv;
-    uint32_t hi = v, li = v, hc = kSelf, lc = kSelf;
-#pragma unroll
-    for (int k = 0; k < NS; ++k) {
-      if (!in_grid<DIM>(g, x, y, z, k)) continue;
-      const uint32_t u = v + slot_offset<DIM>(g, k);
-      const uint64_t ku = okey(ld<kCoherent>(vals + u));
-      if (ku > hk || (ku == hk && u > hi)) {
-        hk = ku;
-        hi = u;
-        hc = k;
-      }
-      if (ku < lk || (ku == lk && u < li)) {
-        lk = ku;
-        li = u;
-        lc = k;
-      }
-    }
-    return hc | (lc << 4);
+  for (int r = 0; r < NR; ++r) {
+    const int k = rank_slot<DIM>(r);
+    ok[r] = k == 15 || interior || in_grid<DIM>(g, x, y, z, k);
+    const uint32_t u = (k == 15 || !ok[r]) ? v : v + slot_offset<DIM>(g, k);
+    key[r] = okey(ld<kCoherent>(vals + u));
   }
+  K hi = 0, lo = ~K(0);
+  uint32_t hc = kSelf, lc = kSelf;
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const uint32_t k = static_cast<uint32_t>(rank_slot<DIM>(r));
+    if (ok[r] && key[r] >= hi) {
+      hi = key[r];
+      hc = k;
+    }
+    if (ok[r] && key[r] < lo) {
+      lo = key[r];
+      lc = k;
+    }
+  }
+  return hc | (lc << 4);
 }
 
 __device__ __forceinline__ bool is_max(uint32_t code) { return (code & 15u) == kSelf; }

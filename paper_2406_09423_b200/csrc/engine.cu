@@ -227,6 +227,11 @@ Workspace& workspace(int device) {
   return *g_ws[device];
 }
 
+// worklists up to this size run inside the leader CTA of k_subloop
+constexpr uint32_t kSmallBatchMax = 4096;
+// worklists above n / kHugeBatchDivisor are run by host-launched streaming kernels
+constexpr uint32_t kHugeBatchDivisor = 4096;
+
 const char* kKindName[4] = {"FPmax", "FPmin", "FNmax", "FNmin"};
 
 // kernel classes of mssz_cu_stats::kernel_ms / kernel_count (MSSZ_CU_PROF_*)
@@ -241,6 +246,8 @@ enum {
   kProfRfix = MSSZ_CU_PROF_RFIX,
   kProfFrontier = MSSZ_CU_PROF_FRONTIER,
   kProfCompact = MSSZ_CU_PROF_COMPACT,
+  kProfLabelFinish = MSSZ_CU_PROF_LABEL_FINISH,
+  kProfFix = MSSZ_CU_PROF_FIX,
 };
 
 // ---------------------------------------------------------------------------
@@ -314,15 +321,30 @@ struct Engine {
     prof_cls.clear();
   }
 
+  // K1 full sweep: 2.5D smem-tiled, chunk of the streamed axis sized for >= 8 CTAs/SM.
   void directions(const T* vals, uint8_t* dir) {
-    dim3 block(128), grid((geo.X + 127) / 128, geo.Y, geo.Z);
     pre(kProfDirections);
-    if (geo.ndims == 2) k_directions<T, 2><<<grid, block, 0, ws.stream>>>(vals, dir, geo);
-    else k_directions<T, 3><<<grid, block, 0, ws.stream>>>(vals, dir, geo);
+    const uint64_t want = static_cast<uint64_t>(ws.sms) * 8;
+    if (geo.ndims == 2) {
+      using DT = DirTile<2>;
+      const uint32_t bx = (geo.X + DT::BX - 1) / DT::BX;
+      uint32_t chunk = static_cast<uint32_t>(std::max<uint64_t>(4, (uint64_t(geo.Y) * bx) / want));
+      chunk = std::min<uint32_t>(chunk, 64);
+      dim3 grid(bx, (geo.Y + chunk - 1) / chunk);
+      k_directions_tiled<T, 2><<<grid, DT::BX * DT::BY, 0, ws.stream>>>(vals, dir, geo, chunk);
+    } else {
+      using DT = DirTile<3>;
+      const uint32_t bx = (geo.X + DT::BX - 1) / DT::BX, by = (geo.Y + DT::BY - 1) / DT::BY;
+      uint32_t chunk =
+          static_cast<uint32_t>(std::max<uint64_t>(4, (uint64_t(geo.Z) * bx * by) / want));
+      chunk = std::min<uint32_t>(chunk, 64);
+      dim3 grid(bx, by, (geo.Z + chunk - 1) / chunk);
+      k_directions_tiled<T, 3><<<grid, DT::BX * DT::BY, 0, ws.stream>>>(vals, dir, geo, chunk);
+    }
     launched(kProfDirections);
   }
 
-  // Pointer-jumping labels; M/m already initialised (codes: k_label_init).
+  // Pointer-jumping labels over arbitrary u32 parent arrays (compute_labels API).
   // Rounds are launched in groups of 4 and the group's last flag is read back.
   void jump_to_fixpoint(uint32_t* M, uint32_t* m) {
     const int cap = bit_width_u64(static_cast<uint64_t>(n()) - 1) + 2;
@@ -350,12 +372,57 @@ struct Engine {
     }
   }
 
-  void labels_from_codes(const uint8_t* dir, uint32_t* M, uint32_t* m) {
+  // Tiled labels (k_label_tile -> exit jumping -> k_label_finish).
+  // finish = false leaves provisional labels (root or resolved exit): lab[lab[v]] is final.
+  void labels_from_codes(const uint8_t* dir, uint32_t* M, uint32_t* m, bool finish) {
     CK(cudaEventRecord(ws.ev[2], ws.stream));
+    CK(cudaMemsetAsync(&ws.ctl->s_count, 0, 2 * sizeof(uint32_t), ws.stream));
+    const uint32_t mark_asc = ws.next_mark;
+    ws.next_mark += 2;
+    uint64_t ntiles;
     pre(kProfLabelInit);
-    k_label_init<<<grid_for(n(), 256, ws.sms, 16), 256, 0, ws.stream>>>(dir, geo, M, m);
+    if (geo.ndims == 2) {
+      using TL = LabelTile<2>;
+      ntiles = uint64_t((geo.X + TL::TX - 1) / TL::TX) * ((geo.Y + TL::TY - 1) / TL::TY);
+      k_label_tile<2><<<static_cast<uint32_t>(ntiles), kLabelTileThreads, 0, ws.stream>>>(
+          dir, geo, M, m, s.fmark, mark_asc, list(2), list(3), &ws.ctl->s_count);
+    } else {
+      using TL = LabelTile<3>;
+      ntiles = uint64_t((geo.X + TL::TX - 1) / TL::TX) * ((geo.Y + TL::TY - 1) / TL::TY) *
+               ((geo.Z + TL::TZ - 1) / TL::TZ);
+      k_label_tile<3><<<static_cast<uint32_t>(ntiles), kLabelTileThreads, 0, ws.stream>>>(
+          dir, geo, M, m, s.fmark, mark_asc, list(2), list(3), &ws.ctl->s_count);
+    }
     launched(kProfLabelInit);
-    jump_to_fixpoint(M, m);
+    // exit chains cross at most ntiles tiles: doubling needs <= bit_width(ntiles)+1 rounds
+    const int cap = bit_width_u64(ntiles) + 2;
+    const uint32_t blocks = grid_for(n() / 4 + 1, 256, ws.sms, 16);
+    int round = 0;
+    for (;;) {
+      const int group = 4;
+      CK(cudaMemsetAsync(ws.ctl->flags, 0, sizeof(uint32_t) * group, ws.stream));
+      for (int r = 0; r < group; ++r) {
+        pre(kProfLabelJump);
+        k_label_exit_jump<<<blocks, 256, 0, ws.stream>>>(M, m, list(2), list(3), &ws.ctl->s_count,
+                                                        &ws.ctl->flags[r]);
+        launched(kProfLabelJump);
+      }
+      uint32_t flags[4];
+      CK(cudaMemcpyAsync(flags, ws.ctl->flags, sizeof flags, cudaMemcpyDeviceToHost, ws.stream));
+      ws.sync();
+      int used = 0;
+      while (used < group && flags[used]) ++used;
+      round += used;
+      st.label_rounds += used < group ? used + 1 : used;
+      if (used < group) break;
+      if (round > cap)
+        fail(MSSZ_CU_ERR_INTERNAL, "path compression exceeded its round cap (corrupt direction field)");
+    }
+    if (finish) {
+      pre(kProfLabelFinish);
+      k_label_finish<<<grid_for(n() / 4 + 1, 256, ws.sms, 16), 256, 0, ws.stream>>>(M, m, n());
+      launched(kProfLabelFinish);
+    }
     CK(cudaEventRecord(ws.ev[3], ws.stream));
     CK(cudaEventSynchronize(ws.ev[3]));
     float ms = 0;
@@ -373,9 +440,9 @@ struct Engine {
     if (coop_blocks) return coop_blocks;
     int occ = 0;
     if (geo.ndims == 2)
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subloop<T, 2>, 512, 0));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subloop<T, 2>, kSubThreads, 0));
     else
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subloop<T, 3>, 512, 0));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subloop<T, 3>, kSubThreads, 0));
     if (occ < 1) fail(MSSZ_CU_ERR_CUDA, "persistent subloop kernel cannot be co-resident");
     coop_blocks = ws.sms * std::min(occ, 2);
     return coop_blocks;
@@ -389,6 +456,60 @@ struct Engine {
     opt.on_batch(host_g.data(), n(), opt.on_batch_user);
   }
 
+  // One huge batch with streaming kernels (see k_subloop): fix_list, full
+  // refresh_directions, detect_kind.  Returns false when the list was empty.
+  // Mirrors one iteration of run_subloop (edit_engine.cpp:255-275).
+  void huge_batch(int kind) {
+    Ctl c = *ws.hctl;  // state handed back by k_subloop
+    const uint32_t nl = c.list_count[cur];
+    ++c.attempted;
+    if (c.attempted > opt.subloop_cap)
+      fail(MSSZ_CU_ERR_NON_CONVERGENCE, "%s subloop exceeded its iteration cap", kKindName[kind]);
+    const uint32_t batch = ws.next_batch;
+    ws.next_batch += 2;
+    const int rule = (kind == 0 || kind == 3) ? 0 : 1;
+    CK(cudaMemsetAsync(&ws.ctl->s_count, 0, 2 * sizeof(uint32_t), ws.stream));
+    pre(kProfFix);
+    k_fix_list<T><<<grid_for(nl, 256, ws.sms, 16), 256, 0, ws.stream>>>(s, s.list[cur], nl, rule, batch);
+    launched(kProfFix);
+    uint32_t applied = 0;
+    CK(cudaMemcpyAsync(&applied, &ws.ctl->s_count, 4, cudaMemcpyDeviceToHost, ws.stream));
+    ws.sync();
+    if (applied == 0 && kind == 1) {
+      pre(kProfFix);
+      k_fix_list<T><<<grid_for(nl, 256, ws.sms, 16), 256, 0, ws.stream>>>(s, s.list[cur], nl, 2, batch + 1);
+      launched(kProfFix);
+      CK(cudaMemcpyAsync(&applied, &ws.ctl->s_count, 4, cudaMemcpyDeviceToHost, ws.stream));
+      ws.sync();
+    }
+    if (applied == 0)
+      fail(MSSZ_CU_ERR_NON_CONVERGENCE, "%s subloop stalled at the float floor", kKindName[kind]);
+    directions(s.g, s.gdir);
+    CK(cudaMemsetAsync(&ws.ctl->list_count[cur ^ 1], 0, sizeof(uint32_t), ws.stream));
+    pre(kProfDetectKind);
+    k_detect_kind<<<grid_for((n() + 15) / 16, 256, ws.sms, 16), 256, 0, ws.stream>>>(
+        s.fdir, s.gdir, n(), kind, s.list[cur ^ 1], &ws.ctl->list_count[cur ^ 1]);
+    launched(kProfDetectKind);
+    ++st.detect_sweeps;
+    ++st.huge_batches;
+    uint32_t next = 0;
+    CK(cudaMemcpyAsync(&next, &ws.ctl->list_count[cur ^ 1], 4, cudaMemcpyDeviceToHost, ws.stream));
+    ws.sync();
+    // hand the loop state back to the persistent kernel
+    cur ^= 1;
+    c.cur = cur;
+    c.list_count[cur] = next;
+    c.list_count[cur ^ 1] = 0;
+    c.iters += 1;
+    c.edits += applied;
+    c.frontier += n();
+    c.s_count = c.f_count = 0;
+    c.status = kStatusOk;
+    *ws.hctl = c;
+    ws.push_ctl();
+    on_batch();
+  }
+
   // run_subloop (edit_engine.cpp:246-278)
   uint64_t run_subloop(int kind) {
     reset_ctl();
@@ -399,18 +520,31 @@ struct Engine {
     launched(kProfDetectKind);
     ++st.detect_sweeps;
     const uint32_t batch_base = ws.next_batch, mark_base = ws.next_mark;
+    // persistent-kernel ids: batch_base + 2*it (+1), mark_base + it, it <= attempted
+    ws.next_batch += static_cast<uint32_t>(2 * std::min<uint64_t>(opt.subloop_cap, 0x7FFFFFF) + 4);
+    ws.next_mark += static_cast<uint32_t>(std::min<uint64_t>(opt.subloop_cap, 0x7FFFFFF) + 2);
     uint64_t cap = opt.subloop_cap;
     uint32_t maxb = opt.on_batch ? 1u : 0xFFFFFFFFu;
-    void* args[] = {&s, &kind, &cap, (void*)&batch_base, (void*)&mark_base, &maxb};
+    uint32_t small_max = kSmallBatchMax;
+    uint32_t huge_min = std::max<uint32_t>(kSmallBatchMax, n() / kHugeBatchDivisor);
+    void* args[] = {&s, &kind, &cap, (void*)&batch_base, (void*)&mark_base, &maxb, &small_max,
+                    &huge_min};
     void* fn = geo.ndims == 2 ? (void*)k_subloop<T, 2> : (void*)k_subloop<T, 3>;
     const int blocks = coop_grid();
     uint64_t seen_iters = 0;
     for (;;) {
+      CK(cudaMemsetAsync(&ws.ctl->cmd_seq, 0, sizeof(uint32_t), ws.stream));
       pre(kProfSubloop);
-      CK(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(512), args, 0, ws.stream));
+      CK(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kSubThreads), args, 0, ws.stream));
       launched(kProfSubloop);
       ws.pull_ctl();
       const Ctl& c = *ws.hctl;
+      cur = c.cur;
+      if (c.status == kStatusHuge) {
+        huge_batch(kind);
+        seen_iters = ws.hctl->iters;
+        continue;
+      }
       if (!opt.on_batch || c.status != kStatusOk) break;
       if (c.iters == seen_iters) break;  // list empty
       seen_iters = c.iters;
@@ -418,8 +552,6 @@ struct Engine {
     }
     const Ctl& c = *ws.hctl;
     cur = c.cur;
-    ws.next_batch += static_cast<uint32_t>(2 * c.attempted + 4);
-    ws.next_mark += static_cast<uint32_t>(c.attempted + 2);
     if (c.status == kStatusCap)
       fail(MSSZ_CU_ERR_NON_CONVERGENCE, "%s subloop exceeded its iteration cap", kKindName[kind]);
     if (c.status == kStatusStall)
@@ -427,6 +559,7 @@ struct Engine {
     st.sub_iterations[kind] += c.iters;
     st.effective_edits += c.edits;
     st.frontier_vertices += c.frontier;
+    st.big_batches += c.big_batches;
     return c.edits;
   }
 
@@ -441,16 +574,16 @@ struct Engine {
   }
 
   uint64_t count_false_critical() {
-    reset_ctl();
-    ws.push_ctl();
+    CK(cudaMemsetAsync(&ws.ctl->counts[0], 0, sizeof(uint64_t), ws.stream));
     pre(kProfDetectAll);
-    k_detect_all<<<grid_for((n() + 15) / 16, 256, ws.sms, 16), 256, 0, ws.stream>>>(
-        s.fdir, s.gdir, n(), ws.ctl->counts, nullptr);
+    k_count_false<<<grid_for(n() / 16 + 1, 256, ws.sms, 16), 256, 0, ws.stream>>>(
+        s.fdir, s.gdir, n(), &ws.ctl->counts[0]);
     launched(kProfDetectAll);
     ++st.detect_sweeps;
-    ws.pull_ctl();
-    const Ctl& c = *ws.hctl;
-    return c.counts[0] + c.counts[1] + c.counts[2] + c.counts[3];
+    uint64_t total = 0;
+    CK(cudaMemcpyAsync(&total, &ws.ctl->counts[0], sizeof total, cudaMemcpyDeviceToHost, ws.stream));
+    ws.sync();
+    return total;
   }
 
   // run_r_loop (edit_engine.cpp:329-366).  Returns true when it stopped on
@@ -459,7 +592,7 @@ struct Engine {
     uint64_t iters = 0;
     for (;;) {
       if (count_false_critical() != 0) return false;
-      labels_from_codes(s.gdir, lab(2), lab(3));
+      labels_from_codes(s.gdir, lab(2), lab(3), false);
       reset_ctl();
       ws.push_ctl();
       const uint32_t batch = ws.next_batch++;
@@ -476,12 +609,16 @@ struct Engine {
       if (applied == 0)
         fail(MSSZ_CU_ERR_NON_CONVERGENCE, "R-loop stalled: every troublemaker is at its floor");
       const uint32_t mark = ws.next_mark++;
-      pre(kProfFrontier);
-      if (geo.ndims == 2)
-        k_frontier<T, 2><<<grid_for(applied, 256, ws.sms, 16), 256, 0, ws.stream>>>(s, applied, mark);
-      else
-        k_frontier<T, 3><<<grid_for(applied, 256, ws.sms, 16), 256, 0, ws.stream>>>(s, applied, mark);
-      launched(kProfFrontier);
+      if (applied > n() / kHugeBatchDivisor) {
+        directions(s.g, s.gdir);  // large batch: one streaming sweep beats 15 RMWs per edit
+      } else {
+        pre(kProfFrontier);
+        if (geo.ndims == 2)
+          k_frontier<T, 2><<<grid_for(applied, 256, ws.sms, 16), 256, 0, ws.stream>>>(s, applied, mark);
+        else
+          k_frontier<T, 3><<<grid_for(applied, 256, ws.sms, 16), 256, 0, ws.stream>>>(s, applied, mark);
+        launched(kProfFrontier);
+      }
       st.effective_edits += applied;
       ++st.r_iterations;
       on_batch();
@@ -515,7 +652,7 @@ struct Engine {
     directions(d_f, ws.fdir.as<uint8_t>());
     directions(s.g, s.gdir);
     CK(cudaEventRecord(ws.ev[1], ws.stream));
-    labels_from_codes(s.fdir, lab(0), lab(1));
+    labels_from_codes(s.fdir, lab(0), lab(1), true);
     {
       float ms = 0;
       CK(cudaEventElapsedTime(&ms, ws.ev[0], ws.ev[1]));
@@ -546,7 +683,7 @@ struct Engine {
     if (!labels_verified) {
       if (count_false_critical() != 0)
         fail(MSSZ_CU_ERR_INTERNAL, "converged with false critical points");
-      labels_from_codes(s.gdir, lab(2), lab(3));
+      labels_from_codes(s.gdir, lab(2), lab(3), false);
       reset_ctl();
       ws.push_ctl();
       pre(kProfRfix);

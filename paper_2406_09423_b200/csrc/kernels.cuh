@@ -27,6 +27,13 @@ struct Ctl {
   uint64_t nonfinite;  // input validation (edit_engine.cpp:390-397)
   uint64_t violations;
   uint32_t flags[64];  // pointer-jumping "changed" flags, one per round
+  uint32_t cmd_seq;    // leader -> worker CTA command word (k_subloop)
+  uint32_t cmd_type;
+  uint32_t cmd_n;
+  uint32_t cmd_cur;
+  uint32_t cmd_it;
+  uint32_t pad_;
+  uint64_t big_batches;  // batches that ran grid-wide
 };
 
 enum : uint32_t {
@@ -34,65 +41,98 @@ enum : uint32_t {
   kStatusCap = 1,          // subloop cap (edit_engine.cpp:258-260)
   kStatusStall = 2,        // "stalled at the float floor" (:269-271)
   kStatusTroubleMax = 3,   // "troublemaker target is an extremum" (:305-306)
+  kStatusHuge = 4,         // k_subloop handed a huge batch back to the host
 };
 
-// ---------------------------------------------------------------------------
-// K1: full direction sweep (compute_directions, mss.cpp:11-30).
-// Grid (ceil(X/128), Y, Z): one thread per vertex, no div/mod; neighbours come
-// through L1/L2 (each value is reused by up to 15 threads of nearby rows).
-template <class T, int DIM>
-__global__ void __launch_bounds__(128) k_directions(const T* __restrict__ vals,
-                                                    uint8_t* __restrict__ dir, Geom g) {
-  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t y = blockIdx.y;
-  const uint32_t z = blockIdx.z;
-  if (x >= g.X) return;
-  const uint32_t v = x + g.X * y + g.XY * z;
-  dir[v] = static_cast<uint8_t>(direction_code<T, DIM, false>(vals, g, v, x, y, z));
-}
+template <class T>
+struct State;
 
 // ---------------------------------------------------------------------------
-// K1b: full detect sweep for one kind (detect_kind, edit_engine.cpp:104-132),
-// 16 vertices per thread from two 16-byte loads, compacted with one atomic per
-// warp.  List order is arbitrary: every consumer is order-independent.
-__global__ void __launch_bounds__(256) k_detect_kind(const uint8_t* __restrict__ fdir,
-                                                     const uint8_t* __restrict__ gdir,
-                                                     uint32_t n, int kind,
-                                                     uint32_t* __restrict__ list,
-                                                     uint32_t* count) {
-  const uint64_t nchunks = (static_cast<uint64_t>(n) + 15) / 16;
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const uint64_t wbase0 = tid & ~uint64_t(31);
-  for (uint64_t wb = wbase0; wb < nchunks; wb += stride) {
-    const uint64_t c = wb + (threadIdx.x & 31);
-    uint32_t mask = 0;
-    if (c < nchunks) {
-      const uint64_t v0 = c * 16;
-      uint8_t fb[16], gb[16];
-      if (v0 + 16 <= n) {
-        *reinterpret_cast<uint4*>(fb) = __ldg(reinterpret_cast<const uint4*>(fdir + v0));
-        *reinterpret_cast<uint4*>(gb) = __ldg(reinterpret_cast<const uint4*>(gdir + v0));
-      } else {
+// K1: full direction sweep (compute_directions, mss.cpp:11-30) for f, f̂ and large batches.  2.5D
+// streaming: a CTA owns a (BX x BY) column of the grid and walks it along the
+// slowest axis with a ring of three shared-memory planes of SoS keys (halo 1),
+// so every value is fetched once from L2/HBM and converted to its key once;
+// each output direction then needs 15 shared-memory reads.
+template <int DIM>
+struct DirTile;
+template <>
+struct DirTile<2> {
+  static constexpr int BX = 256, BY = 1;  // stream along y
+};
+template <>
+struct DirTile<3> {
+  static constexpr int BX = 64, BY = 8;  // stream along z
+};
+
+template <class T, int DIM>
+__global__ void __launch_bounds__(DirTile<DIM>::BX * DirTile<DIM>::BY)
+    k_directions_tiled(const T* __restrict__ vals, uint8_t* __restrict__ dir, Geom g, int chunk) {
+  using K = typename KeyOf<T>::type;
+  constexpr int BX = DirTile<DIM>::BX, BY = DirTile<DIM>::BY;
+  constexpr int HX = BX + 2, HY = DIM == 2 ? 1 : BY + 2;
+  constexpr int NT = BX * BY;
+  constexpr int NR = StencilSize<DIM>::value + 1;
+  __shared__ K ring[3][HY][HX];
+  const int tx = threadIdx.x % BX, ty = threadIdx.x / BX;
+  const int x0 = blockIdx.x * BX;
+  const int y0 = DIM == 2 ? 0 : blockIdx.y * BY;
+  const int S = DIM == 2 ? static_cast<int>(g.Y) : static_cast<int>(g.Z);  // streamed extent
+  const int s0 = (DIM == 2 ? blockIdx.y : blockIdx.z) * chunk;
+  const int s1 = min(s0 + chunk, S);
+  auto load = [&](int sp) {  // plane/row sp of the streamed axis into its ring slot
+    const int slot = (sp + 3) % 3;
+    for (int i = threadIdx.x; i < HX * HY; i += NT) {
+      const int hx = i % HX, hy = i / HX;
+      const int x = x0 + hx - 1, y = DIM == 2 ? sp : y0 + hy - 1;
+      const int z = DIM == 2 ? 0 : sp;
+      K k = 0;
+      if (sp >= 0 && sp < S && x >= 0 && x < static_cast<int>(g.X) && y >= 0 &&
+          y < static_cast<int>(g.Y))
+        k = okey(__ldg(vals + static_cast<uint64_t>(x) + static_cast<uint64_t>(g.X) * y +
+                       static_cast<uint64_t>(g.XY) * z));
+      ring[slot][hy][hx] = k;
+    }
+  };
+  load(s0 - 1);
+  load(s0);
+  const uint32_t x = x0 + tx;
+  const uint32_t y = DIM == 2 ? 0 : y0 + ty;
+  for (int sp = s0; sp < s1; ++sp) {
+    load(sp + 1);
+    __syncthreads();
+    const uint32_t yy = DIM == 2 ? sp : y, zz = DIM == 2 ? 0 : sp;
+    if (x < g.X && yy < g.Y) {
+      const bool interior = x > 0 && x + 1 < g.X && yy > 0 && yy + 1 < g.Y &&
+                            (DIM == 2 || (zz > 0 && zz + 1 < g.Z));
+      K hi = 0, lo = ~K(0);
+      uint32_t hc = kSelf, lc = kSelf;
+      const int slot[3] = {(sp + 2) % 3, sp % 3, (sp + 1) % 3};  // streamed offset -1, 0, +1
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          fb[j] = (v0 + j < n) ? fdir[v0 + j] : 0xFF;
-          gb[j] = (v0 + j < n) ? gdir[v0 + j] : 0xFF;
+      for (int r = 0; r < NR; ++r) {
+        const int k = rank_slot<DIM>(r);
+        int dx = 0, dy = 0, dz = 0;
+        if (k != 15) stencil<DIM>(k, dx, dy, dz);
+        const bool ok = k == 15 || interior || in_grid<DIM>(g, x, yy, zz, k);
+        // streamed axis offset selects the ring slot
+        const int ds = DIM == 2 ? dy : dz;
+        const K key = ring[slot[ds + 1]][DIM == 2 ? 0 : ty + 1 + dy][tx + 1 + dx];
+        if (ok && key >= hi) {
+          hi = key;
+          hc = k;
+        }
+        if (ok && key < lo) {
+          lo = key;
+          lc = k;
         }
       }
-#pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (kind_match(kind, fb[j], gb[j])) mask |= 1u << j;
+      dir[static_cast<uint64_t>(x) + static_cast<uint64_t>(g.X) * yy +
+          static_cast<uint64_t>(g.XY) * zz] = static_cast<uint8_t>(hc | (lc << 4));
     }
-    const uint32_t base = warp_reserve(__popc(mask), count);
-    uint32_t pos = base;
-    while (mask) {
-      const int j = __ffs(mask) - 1;
-      mask &= mask - 1;
-      list[pos++] = static_cast<uint32_t>(c * 16 + j);
-    }
+    __syncthreads();
   }
 }
+
+// K1b (k_detect_kind, the full detect sweep) is defined with the subloop helpers below.
 
 // Counts of the first-match classes (detect_false_critical, edit_engine.cpp:134-158)
 // into ctl->counts; optional per-vertex class bytes for the API export.
@@ -144,6 +184,7 @@ __global__ void __launch_bounds__(256) k_detect_all(const uint8_t* __restrict__ 
 // the R-loop.  rule: 0 = self (FPmax, FNmin), 1 = g's ascending neighbour
 // (FPmin, FNmax; equals g_argmax_neighbor at batch start, edit_engine.cpp:171-185),
 // 2 = f's descending neighbour (FPmin fallback, edit_engine.cpp:187-195, :262-268).
+// Every helper takes (tid, stride) so it runs either grid-wide or inside one CTA.
 template <class T>
 struct State {
   Geom geo;
@@ -180,8 +221,8 @@ __device__ __forceinline__ bool claim_and_lower(const State<T>& s, uint32_t t, u
 
 template <class T>
 __device__ __forceinline__ void fix_batch(const State<T>& s, const uint32_t* __restrict__ list,
-                                          uint32_t n, int rule, uint32_t batch, uint64_t tid,
-                                          uint64_t stride) {
+                                          uint32_t n, int rule, uint32_t batch, uint32_t* s_count,
+                                          uint64_t tid, uint64_t stride) {
   for (uint64_t wb = tid & ~uint64_t(31); wb < n; wb += stride) {
     const uint64_t i = wb + (threadIdx.x & 31);
     bool ok = false;
@@ -193,7 +234,7 @@ __device__ __forceinline__ void fix_batch(const State<T>& s, const uint32_t* __r
       else t = v + s.geo.off[__ldg(s.fdir + v) >> 4];
       ok = claim_and_lower(s, t, batch);
     }
-    warp_append(ok, t, s.S, &s.ctl->s_count);
+    warp_append(ok, t, s.S, s_count);
   }
 }
 
@@ -201,7 +242,7 @@ __device__ __forceinline__ void fix_batch(const State<T>& s, const uint32_t* __r
 // after a batch), each vertex once (fmark dedupe), and collects them in F.
 template <class T, int DIM>
 __device__ __forceinline__ void frontier_update(const State<T>& s, uint32_t ns, uint32_t mark,
-                                                uint64_t tid, uint64_t stride) {
+                                                uint32_t* f_count, uint64_t tid, uint64_t stride) {
   constexpr int NS = StencilSize<DIM>::value;
   for (uint64_t wb = tid & ~uint64_t(31); wb < ns; wb += stride) {
     const uint64_t i = wb + (threadIdx.x & 31);
@@ -227,12 +268,12 @@ __device__ __forceinline__ void frontier_update(const State<T>& s, uint32_t ns, 
           uz = sz + dz;
           u = sv + slot_offset<DIM>(s.geo, k);
         }
-        if (valid && atomicExch(&s.fmark[u], mark) != mark) {
+        if (valid && __ldcg(s.fmark + u) != mark && atomicExch(&s.fmark[u], mark) != mark) {
           mine = true;
           s.gdir[u] = static_cast<uint8_t>(direction_code<T, DIM, true>(s.g, s.geo, u, ux, uy, uz));
         }
       }
-      warp_append(mine, u, s.F, &s.ctl->f_count);
+      warp_append(mine, u, s.F, f_count);
     }
   }
 }
@@ -260,113 +301,245 @@ __device__ __forceinline__ void rebuild_list(const State<T>& s, int kind, const 
   }
 }
 
+// detect_kind over 16 vertices per thread, warp-compacted (edit_engine.cpp:104-132).
+template <bool kCoherent>
+__device__ __forceinline__ void detect_chunks(const uint8_t* __restrict__ fdir,
+                                              const uint8_t* __restrict__ gdir, uint32_t n,
+                                              int kind, uint32_t* __restrict__ list,
+                                              uint32_t* count, uint64_t tid, uint64_t stride) {
+  const uint64_t nchunks = (static_cast<uint64_t>(n) + 15) / 16;
+  for (uint64_t wb = tid & ~uint64_t(31); wb < nchunks; wb += stride) {
+    const uint64_t c = wb + (threadIdx.x & 31);
+    uint32_t mask = 0;
+    if (c < nchunks) {
+      const uint64_t v0 = c * 16;
+      uint8_t fb[16], gb[16];
+      if (v0 + 16 <= n) {
+        *reinterpret_cast<uint4*>(fb) = __ldg(reinterpret_cast<const uint4*>(fdir + v0));
+        *reinterpret_cast<uint4*>(gb) = ld<kCoherent>(reinterpret_cast<const uint4*>(gdir + v0));
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          fb[j] = (v0 + j < n) ? fdir[v0 + j] : 0xFF;
+          gb[j] = (v0 + j < n) ? ld<kCoherent>(gdir + v0 + j) : 0xFF;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (kind_match(kind, fb[j], gb[j])) mask |= 1u << j;
+    }
+    const uint32_t base = warp_reserve(__popc(mask), count);
+    uint32_t pos = base;
+    while (mask) {
+      const int j = __ffs(mask) - 1;
+      mask &= mask - 1;
+      list[pos++] = static_cast<uint32_t>(c * 16 + j);
+    }
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) k_fix_list(State<T> s, const uint32_t* __restrict__ list,
+                                                  uint32_t n, int rule, uint32_t batch) {
+  fix_batch(s, list, n, rule, batch, &s.ctl->s_count,
+            static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x,
+            static_cast<uint64_t>(gridDim.x) * blockDim.x);
+}
+
+__global__ void __launch_bounds__(256) k_detect_kind(const uint8_t* __restrict__ fdir,
+                                                     const uint8_t* __restrict__ gdir,
+                                                     uint32_t n, int kind,
+                                                     uint32_t* __restrict__ list,
+                                                     uint32_t* count) {
+  detect_chunks<false>(fdir, gdir, n, kind, list, count,
+                       static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x,
+                       static_cast<uint64_t>(gridDim.x) * blockDim.x);
+}
+
 // ---------------------------------------------------------------------------
 // Persistent subloop (run_subloop, edit_engine.cpp:246-278): detect → fix →
-// refresh until the kind's list is empty, entirely on the device.  One
-// cooperative launch per subloop invocation; three grid barriers per batch.
+// refresh until the kind's list is empty, entirely on the device, in one
+// cooperative launch per subloop invocation.
+//
+// CTA 0 is the leader.  Batches with at most small_max worklist items run in
+// the leader CTA alone, separated by __syncthreads (most batches touch < 64
+// vertices); the other CTAs sleep on a command word.  Larger
+// batches are broadcast (ctl->cmd_*) and run grid-wide between grid barriers.
+// Worklists above huge_min return to the host (kStatusHuge), which runs that
+// batch with streaming kernels: at that size one full direction sweep + one
+// detect sweep (6 B/vertex) beats ~15 random read-modify-writes per edit.
 // batch ids: batch_base + 2*it (+1 for the FPmin fallback); mark ids: mark_base + it.
+constexpr int kSubThreads = 512;
+enum : uint32_t { kCmdBatch = 1, kCmdExit = 2 };
+
+struct BatchResult {
+  uint32_t applied;
+  uint32_t nf;
+};
+
 template <class T, int DIM>
-__global__ void __launch_bounds__(512, 1)
-    k_subloop(State<T> s, int kind, uint64_t cap, uint32_t batch_base, uint32_t mark_base,
-              uint32_t max_batches) {
-  cg::grid_group grid = cg::this_grid();
+__device__ BatchResult big_batch(const State<T>& s, cg::grid_group& grid, int kind, uint32_t n,
+                                 uint32_t cur, uint32_t it, uint32_t batch_base,
+                                 uint32_t mark_base) {
+  Ctl* ctl = s.ctl;
   const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  const bool leader = tid == 0;
-  Ctl* ctl = s.ctl;
   const int rule = (kind == 0 || kind == 3) ? 0 : 1;
+  const uint32_t batch = batch_base + 2 * it, mark = mark_base + it;
+  fix_batch(s, s.list[cur], n, rule, batch, &ctl->s_count, tid, stride);
+  grid.sync();
+  uint32_t applied = *reinterpret_cast<volatile uint32_t*>(&ctl->s_count);
+  if (applied == 0 && kind == 1) {
+    grid.sync();  // every thread has read applied == 0 before the fallback appends to S
+    fix_batch(s, s.list[cur], n, 2, batch + 1, &ctl->s_count, tid, stride);
+    grid.sync();
+    applied = *reinterpret_cast<volatile uint32_t*>(&ctl->s_count);
+  }
+  if (applied == 0) return {0, 0};
+  frontier_update<T, DIM>(s, applied, mark, &ctl->f_count, tid, stride);
+  grid.sync();
+  const uint32_t nf = *reinterpret_cast<volatile uint32_t*>(&ctl->f_count);
+  rebuild_list(s, kind, s.list[cur], n, s.list[cur ^ 1], &ctl->list_count[cur ^ 1], nf, mark, tid,
+               stride);
+  grid.sync();
+  if (tid == 0) {
+    ctl->s_count = 0;
+    ctl->f_count = 0;
+    ctl->list_count[cur] = 0;
+  }
+  return {applied, nf};
+}
+
+template <class T, int DIM>
+__device__ BatchResult small_batch(const State<T>& s, int kind, uint32_t n, uint32_t cur,
+                                   uint32_t it, uint32_t batch_base, uint32_t mark_base,
+                                   uint32_t* cnt /* smem [3] */) {
+  const uint64_t tid = threadIdx.x, stride = blockDim.x;
+  const int rule = (kind == 0 || kind == 3) ? 0 : 1;
+  const uint32_t batch = batch_base + 2 * it, mark = mark_base + it;
+  fix_batch(s, s.list[cur], n, rule, batch, &cnt[0], tid, stride);
+  __syncthreads();
+  uint32_t applied = *reinterpret_cast<volatile uint32_t*>(&cnt[0]);
+  if (applied == 0 && kind == 1) {
+    __syncthreads();
+    fix_batch(s, s.list[cur], n, 2, batch + 1, &cnt[0], tid, stride);
+    __syncthreads();
+    applied = *reinterpret_cast<volatile uint32_t*>(&cnt[0]);
+  }
+  if (applied == 0) return {0, 0};
+  frontier_update<T, DIM>(s, applied, mark, &cnt[1], tid, stride);
+  __syncthreads();
+  const uint32_t nf = *reinterpret_cast<volatile uint32_t*>(&cnt[1]);
+  rebuild_list(s, kind, s.list[cur], n, s.list[cur ^ 1], &cnt[2], nf, mark, tid, stride);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s.ctl->list_count[cur ^ 1] = cnt[2];
+    s.ctl->list_count[cur] = 0;
+    cnt[0] = cnt[1] = cnt[2] = 0;
+  }
+  __syncthreads();
+  return {applied, nf};
+}
+
+template <class T, int DIM>
+__global__ void __launch_bounds__(kSubThreads, 1)
+    k_subloop(State<T> s, int kind, uint64_t cap, uint32_t batch_base, uint32_t mark_base,
+              uint32_t max_batches, uint32_t small_max, uint32_t huge_min) {
+  cg::grid_group grid = cg::this_grid();
+  Ctl* ctl = s.ctl;
+  __shared__ uint32_t cmd[4];
+  __shared__ uint32_t cnt[3];
+  if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
+  __syncthreads();
+
+  if (blockIdx.x != 0) {  // worker CTAs: join broadcast batches
+    uint32_t seen = 0;
+    for (;;) {
+      if (threadIdx.x == 0) {
+        volatile uint32_t* seq = &ctl->cmd_seq;
+        while (*seq == seen) __nanosleep(100);
+        __threadfence();
+        cmd[0] = *reinterpret_cast<volatile uint32_t*>(&ctl->cmd_type);
+        cmd[1] = *reinterpret_cast<volatile uint32_t*>(&ctl->cmd_n);
+        cmd[2] = *reinterpret_cast<volatile uint32_t*>(&ctl->cmd_cur);
+        cmd[3] = *reinterpret_cast<volatile uint32_t*>(&ctl->cmd_it);
+      }
+      __syncthreads();
+      ++seen;
+      const uint32_t type = cmd[0], n = cmd[1], cur = cmd[2], it = cmd[3];
+      __syncthreads();
+      if (type == kCmdExit) break;
+      big_batch<T, DIM>(s, grid, kind, n, cur, it, batch_base, mark_base);
+    }
+    grid.sync();
+    return;
+  }
 
   uint32_t cur = *reinterpret_cast<volatile uint32_t*>(&ctl->cur);
   uint64_t attempted = *reinterpret_cast<volatile uint64_t*>(&ctl->attempted);
-  uint64_t iters = 0, edits = 0, frontier = 0;
-  uint32_t status = kStatusOk;
-  uint32_t done_batches = 0;
-
+  uint64_t iters = 0, edits = 0, frontier = 0, big = 0;
+  uint32_t status = kStatusOk, done = 0, seq = 0;
   for (;;) {
     const uint32_t n = *reinterpret_cast<volatile uint32_t*>(&ctl->list_count[cur]);
-    if (n == 0 || done_batches >= max_batches) break;
+    if (n == 0 || done >= max_batches) break;
+    if (n > huge_min) {
+      status = kStatusHuge;
+      break;
+    }
     ++attempted;
     if (attempted > cap) {
       status = kStatusCap;
       break;
     }
     const uint32_t it = static_cast<uint32_t>(attempted);
-    const uint32_t batch = batch_base + 2 * it;
-    const uint32_t mark = mark_base + it;
-    if (leader) {
-      ctl->f_count = 0;
-      ctl->list_count[cur ^ 1] = 0;
+    BatchResult r;
+    if (n <= small_max) {
+      r = small_batch<T, DIM>(s, kind, n, cur, it, batch_base, mark_base, cnt);
+    } else {
+      if (threadIdx.x == 0) {
+        ctl->cmd_type = kCmdBatch;
+        ctl->cmd_n = n;
+        ctl->cmd_cur = cur;
+        ctl->cmd_it = it;
+        __threadfence();
+        atomicExch(&ctl->cmd_seq, ++seq);
+      }
+      r = big_batch<T, DIM>(s, grid, kind, n, cur, it, batch_base, mark_base);
+      ++big;
+      __syncthreads();
     }
-    // phase F: fix (fix_list, edit_engine.cpp:197-227)
-    fix_batch(s, s.list[cur], n, rule, batch, tid, stride);
-    grid.sync();
-    uint32_t applied = *reinterpret_cast<volatile uint32_t*>(&ctl->s_count);
-    if (applied == 0 && kind == 1) {
-      grid.sync();  // every thread has read applied == 0 before the fallback appends to S
-      fix_batch(s, s.list[cur], n, 2, batch + 1, tid, stride);
-      grid.sync();
-      applied = *reinterpret_cast<volatile uint32_t*>(&ctl->s_count);
-    }
-    if (applied == 0) {
+    if (r.applied == 0) {
       status = kStatusStall;
       break;
     }
     ++iters;
-    edits += applied;
-    // phase D: refresh directions on S ∪ N(S) (refresh_directions, edit_engine.cpp:88-95)
-    frontier_update<T, DIM>(s, applied, mark, tid, stride);
-    grid.sync();
-    const uint32_t nf = *reinterpret_cast<volatile uint32_t*>(&ctl->f_count);
-    frontier += nf;
-    // phase L: next worklist (detect_kind on the refreshed field)
-    rebuild_list(s, kind, s.list[cur], n, s.list[cur ^ 1], &ctl->list_count[cur ^ 1], nf, mark,
-                 tid, stride);
-    if (leader) ctl->s_count = 0;
-    grid.sync();
+    edits += r.applied;
+    frontier += r.nf;
     cur ^= 1;
-    ++done_batches;
+    ++done;
+  }
+  if (threadIdx.x == 0) {
+    ctl->cmd_type = kCmdExit;
+    __threadfence();
+    atomicExch(&ctl->cmd_seq, ++seq);
   }
   grid.sync();
-  if (leader) {
+  if (threadIdx.x == 0) {
     ctl->cur = cur;
     ctl->attempted = attempted;
     ctl->iters += iters;
     ctl->edits += edits;
     ctl->frontier += frontier;
+    ctl->big_batches += big;
     ctl->status = status;
   }
 }
 
 // ---------------------------------------------------------------------------
-// K3: extremum labels (compute_labels_into, mss.cpp:51-97) as u32 pointer
-// jumping.  Init follows up to kChase direction codes (1-byte, spatially local
-// gathers), then asynchronous in-place doubling rounds.  In-place doubling
-// reaches the same unique fixpoint (the chain terminus) in no more rounds than
-// the reference's round-synchronous version, so its round cap still applies.
-constexpr int kChase = 8;
-
-__global__ void __launch_bounds__(256) k_label_init(const uint8_t* __restrict__ dir, Geom g,
-                                                    uint32_t* __restrict__ M,
-                                                    uint32_t* __restrict__ m) {
-  __shared__ int32_t off[16];
-  if (threadIdx.x < 16) off[threadIdx.x] = g.off[threadIdx.x];
-  __syncthreads();
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t v = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < g.n;
-       v += stride) {
-    const uint32_t c = __ldg(dir + v);
-    uint32_t a = static_cast<uint32_t>(v) + off[c & 15u];
-    uint32_t d = static_cast<uint32_t>(v) + off[c >> 4];
-#pragma unroll
-    for (int h = 1; h < kChase; ++h) {
-      a += off[__ldg(dir + a) & 15u];
-      d += off[__ldg(dir + d) >> 4];
-    }
-    M[v] = a;
-    m[v] = d;
-  }
-}
-
+// K3 (generic): u32 pointer jumping for arbitrary parent arrays (the exported
+// compute_labels API, mss.cpp:51-97).  Asynchronous in-place doubling reaches
+// the same unique fixpoint (the chain terminus) in no more rounds than the
+// reference's round-synchronous version, so its round cap still applies.
 __global__ void __launch_bounds__(256) k_label_jump(uint32_t* __restrict__ M,
                                                     uint32_t* __restrict__ m, uint32_t n,
                                                     uint32_t* flag) {
@@ -388,6 +561,193 @@ __global__ void __launch_bounds__(256) k_label_jump(uint32_t* __restrict__ M,
     }
   }
   if (__any_sync(0xffffffffu, changed) && (threadIdx.x & 31) == 0) *flag = 1;
+}
+
+// ---------------------------------------------------------------------------
+// K3 (tiled): labels in three passes instead of ~log2(path) full-N rounds.
+//  1. k_label_tile: one CTA per 8192-vertex tile resolves every chain inside
+//     the tile by pointer jumping in shared memory.  A vertex's provisional
+//     label is its chain's root (final) or the first vertex OUTSIDE the tile
+//     (an "exit").  Each distinct exit is appended once to E (fmark dedupe).
+//  2. k_label_exit_jump: pointer jumping over E only; an exit's provisional
+//     label is itself a root or another exit, so E closes under lab[].
+//  3. k_label_finish: one gather per vertex, lab[v] = lab[lab[v]].
+// The fixpoint is the chain terminus, identical to the reference's
+// round-synchronous doubling (mss.cpp:60-80).
+template <int DIM>
+struct LabelTile;
+template <>
+struct LabelTile<2> {
+  static constexpr int TX = 128, TY = 64, TZ = 1, LX = 7, LY = 6;
+};
+template <>
+struct LabelTile<3> {
+  static constexpr int TX = 32, TY = 16, TZ = 16, LX = 5, LY = 4;
+};
+constexpr int kLabelTileN = 8192;
+constexpr int kLabelTileThreads = 512;
+
+template <int DIM>
+__global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
+    const uint8_t* __restrict__ dir, Geom g, uint32_t* __restrict__ M, uint32_t* __restrict__ m,
+    uint32_t* __restrict__ mark, uint32_t mark_asc, uint32_t* __restrict__ E_asc,
+    uint32_t* __restrict__ E_desc, uint32_t* counts /* [0] asc, [1] desc */) {
+  using TL = LabelTile<DIM>;
+  constexpr int NS = StencilSize<DIM>::value;
+  constexpr int PER = kLabelTileN / kLabelTileThreads;
+  __shared__ __align__(16) uint8_t sdir[kLabelTileN];
+  __shared__ uint32_t ptr[kLabelTileN];  // (asc local parent) | (desc local parent) << 16
+  __shared__ int8_t sd[3][16];
+  __shared__ int32_t soff[16];
+  if (threadIdx.x < 16) {
+    int dx = 0, dy = 0, dz = 0;
+#pragma unroll
+    for (int k = 0; k < NS; ++k)
+      if (k == static_cast<int>(threadIdx.x)) stencil<DIM>(k, dx, dy, dz);
+    sd[0][threadIdx.x] = static_cast<int8_t>(dx);
+    sd[1][threadIdx.x] = static_cast<int8_t>(dy);
+    sd[2][threadIdx.x] = static_cast<int8_t>(dz);
+    soff[threadIdx.x] = g.off[threadIdx.x];
+  }
+  const uint32_t ntx = (g.X + TL::TX - 1) / TL::TX;
+  const uint32_t nty = (g.Y + TL::TY - 1) / TL::TY;
+  const uint32_t b = blockIdx.x;
+  const uint32_t tx = b % ntx, ty = (b / ntx) % nty, tz = b / (ntx * nty);
+  const uint32_t x0 = tx * TL::TX, y0 = ty * TL::TY, z0 = tz * TL::TZ;
+  const int ex = min(TL::TX, static_cast<int>(g.X - x0));
+  const int ey = min(TL::TY, static_cast<int>(g.Y - y0));
+  const int ez = DIM == 2 ? 1 : min(TL::TZ, static_cast<int>(g.Z - z0));
+  const uint32_t base = x0 + g.X * y0 + g.XY * z0;
+  const bool full = ex == TL::TX && ey == TL::TY && ez == TL::TZ;
+  // dir tile: 16-byte vector loads when rows are 16-byte aligned and whole
+  if (full && (g.X % 16) == 0) {
+    constexpr int VPR = TL::TX / 16;  // uint4 per row
+    for (int q = threadIdx.x; q < kLabelTileN / 16; q += kLabelTileThreads) {
+      const int row = q / VPR, c = q % VPR;
+      const int ly = row & (TL::TY - 1), lz = row / TL::TY;
+      const uint4 w = __ldg(reinterpret_cast<const uint4*>(dir + base + g.X * ly + g.XY * lz) + c);
+      reinterpret_cast<uint4*>(sdir)[q] = w;
+    }
+  } else {
+#pragma unroll 4
+    for (int i = threadIdx.x; i < kLabelTileN; i += kLabelTileThreads) {
+      const int lx = i & (TL::TX - 1), ly = (i >> TL::LX) & (TL::TY - 1), lz = i >> (TL::LX + TL::LY);
+      const bool val = lx < ex && ly < ey && lz < ez;
+      sdir[i] = val ? __ldg(dir + base + lx + g.X * ly + g.XY * lz) : 0xFF;
+    }
+  }
+  __syncthreads();
+  // local parents; a chain that leaves the tile stops at its last inside vertex
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const int i = threadIdx.x + j * kLabelTileThreads;
+    const int lx = i & (TL::TX - 1), ly = (i >> TL::LX) & (TL::TY - 1), lz = i >> (TL::LX + TL::LY);
+    const bool val = lx < ex && ly < ey && lz < ez;
+    const uint32_t code = sdir[i];
+    uint32_t pr = static_cast<uint32_t>(i) | (static_cast<uint32_t>(i) << 16);
+    if (val) {
+#pragma unroll
+      for (int fam = 0; fam < 2; ++fam) {
+        const uint32_t c = (code >> (4 * fam)) & 15u;
+        if (c == kSelf) continue;
+        const int nx = lx + sd[0][c], ny = ly + sd[1][c], nz = lz + sd[2][c];
+        if (nx >= 0 && nx < ex && ny >= 0 && ny < ey && nz >= 0 && nz < ez) {
+          const uint32_t p = nx + (ny << TL::LX) + (nz << (TL::LX + TL::LY));
+          pr = fam ? ((pr & 0xFFFFu) | (p << 16)) : ((pr & 0xFFFF0000u) | p);
+        }
+      }
+    }
+    ptr[i] = pr;
+  }
+  __syncthreads();
+  // in-place doubling on both families at once
+  for (;;) {
+    bool changed = false;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int i = threadIdx.x + j * kLabelTileThreads;
+      const uint32_t p = ptr[i];
+      const uint32_t np = (ptr[p & 0xFFFFu] & 0xFFFFu) | (ptr[p >> 16] & 0xFFFF0000u);
+      if (np != p) {
+        ptr[i] = np;
+        changed = true;
+      }
+    }
+    if (!__syncthreads_or(changed)) break;
+  }
+  // provisional labels (root, or first vertex outside the tile) + distinct exits
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const int i = threadIdx.x + j * kLabelTileThreads;
+    const int lx = i & (TL::TX - 1), ly = (i >> TL::LX) & (TL::TY - 1), lz = i >> (TL::LX + TL::LY);
+    const bool val = lx < ex && ly < ey && lz < ez;
+    const uint32_t p = ptr[i];
+    bool fresh[2] = {false, false};
+    uint32_t e[2] = {0, 0};
+    if (val) {
+      const uint32_t gi = base + lx + g.X * ly + g.XY * lz;
+#pragma unroll
+      for (int fam = 0; fam < 2; ++fam) {
+        const int t = fam ? (p >> 16) : (p & 0xFFFFu);
+        const uint32_t c = (sdir[t] >> (4 * fam)) & 15u;
+        const int tlx = t & (TL::TX - 1), tly = (t >> TL::LX) & (TL::TY - 1),
+                  tlz = t >> (TL::LX + TL::LY);
+        const uint32_t res = base + tlx + g.X * tly + g.XY * tlz + soff[c];  // soff[15] = 0
+        (fam ? m : M)[gi] = res;
+        if (t == i && c != kSelf) {  // this chain leaves the tile here
+          e[fam] = res;
+          const uint32_t mk = mark_asc + fam;
+          fresh[fam] = __ldcg(mark + res) != mk && atomicExch(mark + res, mk) != mk;
+        }
+      }
+    }
+    warp_append(fresh[0], e[0], E_asc, counts + 0);
+    warp_append(fresh[1], e[1], E_desc, counts + 1);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_label_exit_jump(uint32_t* __restrict__ M,
+                                                         uint32_t* __restrict__ m,
+                                                         const uint32_t* __restrict__ Ea,
+                                                         const uint32_t* __restrict__ Ed,
+                                                         const uint32_t* counts, uint32_t* flag) {
+  const uint32_t na = counts[0], nd = counts[1];
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  bool changed = false;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+       i < static_cast<uint64_t>(na) + nd; i += stride) {
+    uint32_t* lab = i < na ? M : m;
+    const uint32_t e = i < na ? Ea[i] : Ed[i - na];
+    const uint32_t l = lab[e];
+    const uint32_t ll = lab[l];
+    if (ll != l) {
+      lab[e] = ll;
+      changed = true;
+    }
+  }
+  if (__any_sync(0xffffffffu, changed) && (threadIdx.x & 31) == 0) *flag = 1;
+}
+
+__global__ void __launch_bounds__(256) k_label_finish(uint32_t* __restrict__ M,
+                                                      uint32_t* __restrict__ m, uint32_t n) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t n4 = n / 4;
+  for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n4;
+       q += stride) {
+    uint4 a = reinterpret_cast<const uint4*>(M)[q];
+    uint4 d = reinterpret_cast<const uint4*>(m)[q];
+    const uint32_t a2[4] = {M[a.x], M[a.y], M[a.z], M[a.w]};
+    const uint32_t d2[4] = {m[d.x], m[d.y], m[d.z], m[d.w]};
+    if (a2[0] != a.x || a2[1] != a.y || a2[2] != a.z || a2[3] != a.w)
+      reinterpret_cast<uint4*>(M)[q] = make_uint4(a2[0], a2[1], a2[2], a2[3]);
+    if (d2[0] != d.x || d2[1] != d.y || d2[2] != d.z || d2[3] != d.w)
+      reinterpret_cast<uint4*>(m)[q] = make_uint4(d2[0], d2[1], d2[2], d2[3]);
+  }
+  for (uint64_t v = n4 * 4 + static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < n;
+       v += stride) {
+    M[v] = M[M[v]];
+    m[v] = m[m[v]];
+  }
 }
 
 // Generic u64 parent arrays (the exported compute_labels API): copy to u32.
@@ -421,38 +781,68 @@ __global__ void k_u32_to_u64(const uint32_t* __restrict__ in, uint64_t* __restri
 // and one full sweep finds it without walking.  Targets are claimed once and
 // lowered from the pre-batch g, which is the reference's batch semantics (claim
 // stamps, then lower_step over the deduplicated targets).
+//
+// The g labels arrive provisional (k_label_tile + exit jumping, no finish
+// pass): lab[v] is a root or a resolved exit, so lab[lab[v]] is final.  Only
+// divergent vertices need their label, so the full-N finish pass is skipped.
+// ctl->mism counts divergent mismatched vertices: it is zero exactly when no
+// vertex is mismatched (the walk argument above), which is the reference's
+// collect_mismatched() == 0 test.
 template <class T>
 __global__ void __launch_bounds__(256) k_rfix(State<T> s, uint32_t batch) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   uint32_t mism = 0;
   const uint32_t n = s.geo.n;
-  for (uint64_t wb = tid & ~uint64_t(31); wb < n; wb += stride) {
-    const uint64_t v = wb + (threadIdx.x & 31);
-    bool oka = false, okd = false;
-    uint32_t ta = 0, td = 0;
-    if (v < n) {
-      const uint32_t fc = __ldg(s.fdir + v), gc = __ldg(s.gdir + v);
-      const bool mM = __ldg(s.gM + v) != __ldg(s.fM + v);
-      const bool mm = __ldg(s.gm + v) != __ldg(s.fm + v);
-      mism += (mM || mm) ? 1u : 0u;
-      if (mM && (gc & 15u) != (fc & 15u)) {
-        if ((gc & 15u) == kSelf) atomicExch(&s.ctl->status, kStatusTroubleMax);
-        else {
-          ta = static_cast<uint32_t>(v) + s.geo.off[gc & 15u];
-          oka = claim_and_lower(s, ta, batch);
-        }
-      }
-      if (mm && (gc >> 4) != (fc >> 4)) {
-        if ((fc >> 4) == kSelf) atomicExch(&s.ctl->status, kStatusTroubleMax);
-        else {
-          td = static_cast<uint32_t>(v) + s.geo.off[fc >> 4];
-          okd = claim_and_lower(s, td, batch);
+  const uint64_t nq = (static_cast<uint64_t>(n) + 3) / 4;
+  for (uint64_t wb = tid & ~uint64_t(31); wb < nq; wb += stride) {
+    const uint64_t q = wb + (threadIdx.x & 31);
+    uint32_t fw = 0xFFFFFFFFu, gw = 0xFFFFFFFFu;
+    if (q < nq) {
+      if (q * 4 + 4 <= n) {
+        fw = __ldg(reinterpret_cast<const uint32_t*>(s.fdir) + q);
+        gw = __ldg(reinterpret_cast<const uint32_t*>(s.gdir) + q);
+      } else {
+        fw = gw = 0;
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t fb = q * 4 + j < n ? s.fdir[q * 4 + j] : 0xFFu;
+          const uint32_t gb = q * 4 + j < n ? s.gdir[q * 4 + j] : 0xFFu;
+          fw |= fb << (8 * j);
+          gw |= gb << (8 * j);
         }
       }
     }
-    warp_append(oka, ta, s.S, &s.ctl->s_count);
-    warp_append(okd, td, s.S, &s.ctl->s_count);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t v = static_cast<uint32_t>(q * 4 + j);
+      const uint32_t fc = (fw >> (8 * j)) & 0xFFu, gc = (gw >> (8 * j)) & 0xFFu;
+      bool oka = false, okd = false;
+      uint32_t ta = 0, td = 0;
+      if ((gc & 15u) != (fc & 15u)) {  // ascending line diverges at v
+        const uint32_t gl = __ldg(s.gM + v);
+        if (__ldg(s.gM + gl) != __ldg(s.fM + v)) {
+          ++mism;
+          if ((gc & 15u) == kSelf) atomicExch(&s.ctl->status, kStatusTroubleMax);
+          else {
+            ta = v + s.geo.off[gc & 15u];
+            oka = claim_and_lower(s, ta, batch);
+          }
+        }
+      }
+      if ((gc >> 4) != (fc >> 4)) {  // descending line diverges at v
+        const uint32_t gl = __ldg(s.gm + v);
+        if (__ldg(s.gm + gl) != __ldg(s.fm + v)) {
+          ++mism;
+          if ((fc >> 4) == kSelf) atomicExch(&s.ctl->status, kStatusTroubleMax);
+          else {
+            td = v + s.geo.off[fc >> 4];
+            okd = claim_and_lower(s, td, batch);
+          }
+        }
+      }
+      warp_append(oka, ta, s.S, &s.ctl->s_count);
+      warp_append(okd, td, s.S, &s.ctl->s_count);
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mism += __shfl_xor_sync(0xffffffffu, mism, o);
@@ -461,12 +851,47 @@ __global__ void __launch_bounds__(256) k_rfix(State<T> s, uint32_t batch) {
               static_cast<unsigned long long>(mism));
 }
 
+// Gate of the R-loop (detect_false_critical().empty(), edit_engine.cpp:338):
+// a vertex is a false critical point of some kind iff its max flag or its min
+// flag differs between f and g.  SWAR over 16 codes per thread.
+__device__ __forceinline__ uint32_t zero_bytes(uint32_t u) {  // 0x80 per zero byte, exact
+  const uint32_t y = (u & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;
+  return ~(y | u | 0x7F7F7F7Fu);
+}
+__device__ __forceinline__ uint32_t false_cp_bytes(uint32_t f, uint32_t g) {
+  const uint32_t fmx = zero_bytes(~f & 0x0F0F0F0Fu), gmx = zero_bytes(~g & 0x0F0F0F0Fu);
+  const uint32_t fmn = zero_bytes(~f & 0xF0F0F0F0u), gmn = zero_bytes(~g & 0xF0F0F0F0u);
+  return (fmx ^ gmx) | (fmn ^ gmn);
+}
+
+__global__ void __launch_bounds__(256) k_count_false(const uint8_t* __restrict__ fdir,
+                                                     const uint8_t* __restrict__ gdir, uint32_t n,
+                                                     uint64_t* total) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t n16 = n / 16;
+  uint32_t c = 0;
+  for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n16;
+       q += stride) {
+    const uint4 f = __ldg(reinterpret_cast<const uint4*>(fdir) + q);
+    const uint4 gg = __ldg(reinterpret_cast<const uint4*>(gdir) + q);
+    c += __popc(false_cp_bytes(f.x, gg.x)) + __popc(false_cp_bytes(f.y, gg.y)) +
+         __popc(false_cp_bytes(f.z, gg.z)) + __popc(false_cp_bytes(f.w, gg.w));
+  }
+  for (uint64_t v = n16 * 16 + static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+       v < n; v += stride)
+    c += __popc(false_cp_bytes(fdir[v], gdir[v]) & 0xFFu);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c)
+    atomicAdd(reinterpret_cast<unsigned long long*>(total), static_cast<unsigned long long>(c));
+}
+
 // Non-persistent frontier refresh (after an R batch).
 template <class T, int DIM>
 __global__ void __launch_bounds__(256) k_frontier(State<T> s, uint32_t ns, uint32_t mark) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  frontier_update<T, DIM>(s, ns, mark, tid, stride);
+  frontier_update<T, DIM>(s, ns, mark, &s.ctl->f_count, tid, stride);
 }
 
 // ---------------------------------------------------------------------------
