@@ -381,7 +381,8 @@ def main():
                        "effective_edits": st.effective_edits, "touched": st.touched,
                        "label_passes": st.label_passes, "label_rounds": st.label_rounds,
                        "detect_sweeps": st.detect_sweeps,
-                       "frontier_vertices": st.frontier_vertices},
+                       "frontier_vertices": st.frontier_vertices,
+                       "big_batches": st.big_batches, "huge_batches": st.huge_batches},
         "kernel_profile_ms_per_step": prof,
     }
     if dist.rank == 0:

@@ -170,6 +170,10 @@ struct Workspace {
     CK(cudaMalloc(&ctl, sizeof(Ctl)));
     CK(cudaMallocHost(&hctl, sizeof(Ctl)));
     for (auto& e : ev) CK(cudaEventCreate(&e));
+    CK(cudaFuncSetAttribute(k_label_tile<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(label_tile_smem<2>())));
+    CK(cudaFuncSetAttribute(k_label_tile<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(label_tile_smem<3>())));
   }
   void release() {
     for (DevBuf* b : {&f, &g, &fdir, &gdir, &touched, &stamp, &fmark, &lab, &lists, &tiles})
@@ -230,7 +234,7 @@ Workspace& workspace(int device) {
 // worklists up to this size run inside the leader CTA of k_subloop
 constexpr uint32_t kSmallBatchMax = 4096;
 // worklists above n / kHugeBatchDivisor are run by host-launched streaming kernels
-constexpr uint32_t kHugeBatchDivisor = 4096;
+uint32_t kHugeBatchDivisor = 64;  // tunable via MSSZ_HUGE_DIVISOR (experiments)
 
 const char* kKindName[4] = {"FPmax", "FPmin", "FNmax", "FNmin"};
 
@@ -384,40 +388,40 @@ struct Engine {
     if (geo.ndims == 2) {
       using TL = LabelTile<2>;
       ntiles = uint64_t((geo.X + TL::TX - 1) / TL::TX) * ((geo.Y + TL::TY - 1) / TL::TY);
-      k_label_tile<2><<<static_cast<uint32_t>(ntiles), kLabelTileThreads, 0, ws.stream>>>(
+      k_label_tile<2><<<static_cast<uint32_t>(ntiles), kLabelTileThreads, label_tile_smem<2>(),
+                        ws.stream>>>(
           dir, geo, M, m, s.fmark, mark_asc, list(2), list(3), &ws.ctl->s_count);
     } else {
       using TL = LabelTile<3>;
       ntiles = uint64_t((geo.X + TL::TX - 1) / TL::TX) * ((geo.Y + TL::TY - 1) / TL::TY) *
                ((geo.Z + TL::TZ - 1) / TL::TZ);
-      k_label_tile<3><<<static_cast<uint32_t>(ntiles), kLabelTileThreads, 0, ws.stream>>>(
+      k_label_tile<3><<<static_cast<uint32_t>(ntiles), kLabelTileThreads, label_tile_smem<3>(),
+                        ws.stream>>>(
           dir, geo, M, m, s.fmark, mark_asc, list(2), list(3), &ws.ctl->s_count);
     }
     launched(kProfLabelInit);
-    // exit chains cross at most ntiles tiles: doubling needs <= bit_width(ntiles)+1 rounds
-    const int cap = bit_width_u64(ntiles) + 2;
-    const uint32_t blocks = grid_for(n() / 4 + 1, 256, ws.sms, 16);
-    int round = 0;
-    for (;;) {
-      const int group = 4;
-      CK(cudaMemsetAsync(ws.ctl->flags, 0, sizeof(uint32_t) * group, ws.stream));
-      for (int r = 0; r < group; ++r) {
-        pre(kProfLabelJump);
-        k_label_exit_jump<<<blocks, 256, 0, ws.stream>>>(M, m, list(2), list(3), &ws.ctl->s_count,
-                                                        &ws.ctl->flags[r]);
-        launched(kProfLabelJump);
-      }
-      uint32_t flags[4];
-      CK(cudaMemcpyAsync(flags, ws.ctl->flags, sizeof flags, cudaMemcpyDeviceToHost, ws.stream));
-      ws.sync();
-      int used = 0;
-      while (used < group && flags[used]) ++used;
-      round += used;
-      st.label_rounds += used < group ? used + 1 : used;
-      if (used < group) break;
-      if (round > cap)
-        fail(MSSZ_CU_ERR_INTERNAL, "path compression exceeded its round cap (corrupt direction field)");
+    // exit chains cross at most ntiles tiles: doubling needs <= bit_width(ntiles)+1
+    // rounds.  Rounds are launched blind (no host sync); each compacts the
+    // unresolved exits into the other list pair, so late rounds are near-empty.
+    const int rounds = bit_width_u64(ntiles) + 2;
+    const uint32_t blocks = grid_for(n() / 8 + 1, 256, ws.sms, 16);
+    uint32_t* cnt[2] = {&ws.ctl->s_count, &ws.ctl->list_count[0]};  // (asc, desc) pairs
+    uint32_t* la[2] = {list(2), list(0)};
+    uint32_t* ld[2] = {list(3), list(1)};
+    for (int r = 0; r < rounds; ++r) {
+      const int a = r & 1, b2 = a ^ 1;
+      CK(cudaMemsetAsync(cnt[b2], 0, 2 * sizeof(uint32_t), ws.stream));
+      pre(kProfLabelJump);
+      k_label_exit_jump<<<blocks, 256, 0, ws.stream>>>(M, m, la[a], ld[a], la[b2], ld[b2], cnt[a],
+                                                      cnt[b2]);
+      launched(kProfLabelJump);
     }
+    st.label_rounds += rounds;
+    uint32_t left[2];
+    CK(cudaMemcpyAsync(left, cnt[rounds & 1], sizeof left, cudaMemcpyDeviceToHost, ws.stream));
+    ws.sync();
+    if (left[0] || left[1])
+      fail(MSSZ_CU_ERR_INTERNAL, "path compression exceeded its round cap (corrupt direction field)");
     if (finish) {
       pre(kProfLabelFinish);
       k_label_finish<<<grid_for(n() / 4 + 1, 256, ws.sms, 16), 256, 0, ws.stream>>>(M, m, n());
@@ -438,6 +442,7 @@ struct Engine {
 
   int coop_grid() {
     if (coop_blocks) return coop_blocks;
+    if (const char* h = std::getenv("MSSZ_HUGE_DIVISOR")) kHugeBatchDivisor = std::max(1, std::atoi(h));
     int occ = 0;
     if (geo.ndims == 2)
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subloop<T, 2>, kSubThreads, 0));
@@ -459,14 +464,13 @@ struct Engine {
   // One huge batch with streaming kernels (see k_subloop): fix_list, full
   // refresh_directions, detect_kind.  Returns false when the list was empty.
   // Mirrors one iteration of run_subloop (edit_engine.cpp:255-275).
-  void huge_batch(int kind) {
+  void huge_batch(int kind, uint32_t batch_base) {
     Ctl c = *ws.hctl;  // state handed back by k_subloop
     const uint32_t nl = c.list_count[cur];
     ++c.attempted;
     if (c.attempted > opt.subloop_cap)
       fail(MSSZ_CU_ERR_NON_CONVERGENCE, "%s subloop exceeded its iteration cap", kKindName[kind]);
-    const uint32_t batch = ws.next_batch;
-    ws.next_batch += 2;
+    const uint32_t batch = batch_base + 2 * static_cast<uint32_t>(c.attempted);  // k_subloop's scheme
     const int rule = (kind == 0 || kind == 3) ? 0 : 1;
     CK(cudaMemsetAsync(&ws.ctl->s_count, 0, 2 * sizeof(uint32_t), ws.stream));
     pre(kProfFix);
@@ -520,9 +524,16 @@ struct Engine {
     launched(kProfDetectKind);
     ++st.detect_sweeps;
     const uint32_t batch_base = ws.next_batch, mark_base = ws.next_mark;
-    // persistent-kernel ids: batch_base + 2*it (+1), mark_base + it, it <= attempted
-    ws.next_batch += static_cast<uint32_t>(2 * std::min<uint64_t>(opt.subloop_cap, 0x7FFFFFF) + 4);
-    ws.next_mark += static_cast<uint32_t>(std::min<uint64_t>(opt.subloop_cap, 0x7FFFFFF) + 2);
+    // stamp ids must never be reused, also when this subloop raises
+    struct IdGuard {
+      Workspace& ws;
+      uint32_t bb, mb;
+      ~IdGuard() {
+        const uint32_t it = static_cast<uint32_t>(ws.hctl->attempted) + 2;
+        ws.next_batch = std::max(ws.next_batch, bb + 2 * it + 4);
+        ws.next_mark = std::max(ws.next_mark, mb + it + 2);
+      }
+    } id_guard{ws, batch_base, mark_base};
     uint64_t cap = opt.subloop_cap;
     uint32_t maxb = opt.on_batch ? 1u : 0xFFFFFFFFu;
     uint32_t small_max = kSmallBatchMax;
@@ -541,7 +552,7 @@ struct Engine {
       const Ctl& c = *ws.hctl;
       cur = c.cur;
       if (c.status == kStatusHuge) {
-        huge_batch(kind);
+        huge_batch(kind, batch_base);
         seen_iters = ws.hctl->iters;
         continue;
       }

@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(DirTile<DIM>::BX * DirTile<DIM>::BY)
   constexpr int BX = DirTile<DIM>::BX, BY = DirTile<DIM>::BY;
   constexpr int HX = BX + 2, HY = DIM == 2 ? 1 : BY + 2;
   constexpr int NT = BX * BY;
+  constexpr int PL = (HX * HY + NT - 1) / NT;  // plane elements per thread
   constexpr int NR = StencilSize<DIM>::value + 1;
   __shared__ K ring[3][HY][HX];
   const int tx = threadIdx.x % BX, ty = threadIdx.x / BX;
@@ -79,56 +80,88 @@ __global__ void __launch_bounds__(DirTile<DIM>::BX * DirTile<DIM>::BY)
   const int S = DIM == 2 ? static_cast<int>(g.Y) : static_cast<int>(g.Z);  // streamed extent
   const int s0 = (DIM == 2 ? blockIdx.y : blockIdx.z) * chunk;
   const int s1 = min(s0 + chunk, S);
-  auto load = [&](int sp) {  // plane/row sp of the streamed axis into its ring slot
+  // this thread's share of every halo plane: flat element ids, validity, base offset
+  int64_t eoff[PL];
+  bool evalid[PL];
+#pragma unroll
+  for (int j = 0; j < PL; ++j) {
+    const int i = threadIdx.x + j * NT;
+    const int hx = i % HX, hy = i / HX;
+    const int x = x0 + hx - 1, y = DIM == 2 ? 0 : y0 + hy - 1;
+    evalid[j] = i < HX * HY && x >= 0 && x < static_cast<int>(g.X) && y >= 0 &&
+                y < static_cast<int>(g.Y);
+    eoff[j] = evalid[j] ? static_cast<int64_t>(x) + static_cast<int64_t>(g.X) * y : 0;
+  }
+  const int64_t pstride = DIM == 2 ? static_cast<int64_t>(g.X) : static_cast<int64_t>(g.XY);
+  // register pipeline: pre[u] holds a plane D steps ahead, so ~D planes of
+  // loads are in flight per thread while the current plane is evaluated
+  constexpr int D = 2;
+  K pre[D][PL];
+  auto fetch = [&](int sp, K* dst) {  // issue the loads of plane sp (no wait)
+#pragma unroll
+    for (int j = 0; j < PL; ++j)
+      dst[j] = (evalid[j] && sp >= 0 && sp < S) ? okey(__ldg(vals + eoff[j] + pstride * sp)) : K(0);
+  };
+  auto commit = [&](int sp, const K* src) {
     const int slot = (sp + 3) % 3;
-    for (int i = threadIdx.x; i < HX * HY; i += NT) {
-      const int hx = i % HX, hy = i / HX;
-      const int x = x0 + hx - 1, y = DIM == 2 ? sp : y0 + hy - 1;
-      const int z = DIM == 2 ? 0 : sp;
-      K k = 0;
-      if (sp >= 0 && sp < S && x >= 0 && x < static_cast<int>(g.X) && y >= 0 &&
-          y < static_cast<int>(g.Y))
-        k = okey(__ldg(vals + static_cast<uint64_t>(x) + static_cast<uint64_t>(g.X) * y +
-                       static_cast<uint64_t>(g.XY) * z));
-      ring[slot][hy][hx] = k;
+#pragma unroll
+    for (int j = 0; j < PL; ++j) {
+      const int i = threadIdx.x + j * NT;
+      if (i < HX * HY) (&ring[slot][0][0])[i] = src[j];
     }
   };
-  load(s0 - 1);
-  load(s0);
+  fetch(s0 - 1, pre[0]);
+  commit(s0 - 1, pre[0]);
+  fetch(s0, pre[1]);
+  commit(s0, pre[1]);
+#pragma unroll
+  for (int u = 0; u < D; ++u) fetch(s0 + 1 + u, pre[u]);
   const uint32_t x = x0 + tx;
   const uint32_t y = DIM == 2 ? 0 : y0 + ty;
-  for (int sp = s0; sp < s1; ++sp) {
-    load(sp + 1);
+  for (int sp0 = s0; sp0 < s1; sp0 += D) {
+#pragma unroll
+  for (int u = 0; u < D; ++u) {
+    const int sp = sp0 + u;
+    if (sp >= s1) break;
+    commit(sp + 1, pre[u]);
     __syncthreads();
+    fetch(sp + 1 + D, pre[u]);  // in flight while planes sp .. sp+D-1 are evaluated
     const uint32_t yy = DIM == 2 ? sp : y, zz = DIM == 2 ? 0 : sp;
     if (x < g.X && yy < g.Y) {
-      const bool interior = x > 0 && x + 1 < g.X && yy > 0 && yy + 1 < g.Y &&
-                            (DIM == 2 || (zz > 0 && zz + 1 < g.Z));
-      K hi = 0, lo = ~K(0);
       uint32_t hc = kSelf, lc = kSelf;
-      const int slot[3] = {(sp + 2) % 3, sp % 3, (sp + 1) % 3};  // streamed offset -1, 0, +1
+      // Halo / out-of-grid cells hold key 0 (valid keys are >= 0x00800000...):
+      // 0 never wins the ascending max, and key - 1 wraps to ~0 so it never
+      // wins the descending min either -- no bounds tests per slot.
+      const int row = (DIM == 2 ? 0 : ty + 1) * HX + tx + 1;
+      const K* pl[3] = {&ring[(sp + 2) % 3][0][0] + row, &ring[sp % 3][0][0] + row,
+                        &ring[(sp + 1) % 3][0][0] + row};
+      K key[NR];
 #pragma unroll
       for (int r = 0; r < NR; ++r) {
         const int k = rank_slot<DIM>(r);
         int dx = 0, dy = 0, dz = 0;
         if (k != 15) stencil<DIM>(k, dx, dy, dz);
-        const bool ok = k == 15 || interior || in_grid<DIM>(g, x, yy, zz, k);
-        // streamed axis offset selects the ring slot
         const int ds = DIM == 2 ? dy : dz;
-        const K key = ring[slot[ds + 1]][DIM == 2 ? 0 : ty + 1 + dy][tx + 1 + dx];
-        if (ok && key >= hi) {
-          hi = key;
-          hc = k;
-        }
-        if (ok && key < lo) {
-          lo = key;
-          lc = k;
-        }
+        key[r] = pl[ds + 1][(DIM == 2 ? 0 : dy * HX) + dx];
+      }
+      K hi = key[0], lo = key[0] - 1;
+#pragma unroll
+      for (int r = 1; r < NR; ++r) {
+        hi = max(hi, key[r]);
+        lo = min(lo, key[r] - 1);
+      }
+      // ties: ascending keeps the highest index (last in rank order),
+      // descending the lowest index (first in rank order)
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        if (key[r] == hi) hc = rank_slot<DIM>(r);
+        if (key[NR - 1 - r] - 1 == lo) lc = rank_slot<DIM>(NR - 1 - r);
       }
       dir[static_cast<uint64_t>(x) + static_cast<uint64_t>(g.X) * yy +
           static_cast<uint64_t>(g.XY) * zz] = static_cast<uint8_t>(hc | (lc << 4));
     }
     __syncthreads();
+  }
   }
 }
 
@@ -301,6 +334,24 @@ __device__ __forceinline__ void rebuild_list(const State<T>& s, int kind, const 
   }
 }
 
+// SWAR helpers on 4 packed direction codes: 0x80 in every byte whose
+// nibble is all ones (SELF), exact per byte.
+__device__ __forceinline__ uint32_t zero_bytes(uint32_t u) {
+  const uint32_t y = (u & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;
+  return ~(y | u | 0x7F7F7F7Fu);
+}
+__device__ __forceinline__ uint32_t kind_bytes(int kind, uint32_t f, uint32_t g) {
+  switch (kind) {
+    case 0: return zero_bytes(~g & 0x0F0F0F0Fu) & ~zero_bytes(~f & 0x0F0F0F0Fu);   // FPmax
+    case 1: return zero_bytes(~g & 0xF0F0F0F0u) & ~zero_bytes(~f & 0xF0F0F0F0u);   // FPmin
+    case 2: return zero_bytes(~f & 0x0F0F0F0Fu) & ~zero_bytes(~g & 0x0F0F0F0Fu);   // FNmax
+    default: return zero_bytes(~f & 0xF0F0F0F0u) & ~zero_bytes(~g & 0xF0F0F0F0u);  // FNmin
+  }
+}
+__device__ __forceinline__ uint32_t bytes_to_nibble(uint32_t x) {  // 0x80 flags -> 4-bit mask
+  return (((x >> 7) & 0x01010101u) * 0x01020408u) >> 24 & 0xFu;
+}
+
 // detect_kind over 16 vertices per thread, warp-compacted (edit_engine.cpp:104-132).
 template <bool kCoherent>
 __device__ __forceinline__ void detect_chunks(const uint8_t* __restrict__ fdir,
@@ -313,20 +364,18 @@ __device__ __forceinline__ void detect_chunks(const uint8_t* __restrict__ fdir,
     uint32_t mask = 0;
     if (c < nchunks) {
       const uint64_t v0 = c * 16;
-      uint8_t fb[16], gb[16];
       if (v0 + 16 <= n) {
-        *reinterpret_cast<uint4*>(fb) = __ldg(reinterpret_cast<const uint4*>(fdir + v0));
-        *reinterpret_cast<uint4*>(gb) = ld<kCoherent>(reinterpret_cast<const uint4*>(gdir + v0));
+        const uint4 f = __ldg(reinterpret_cast<const uint4*>(fdir + v0));
+        const uint4 g = ld<kCoherent>(reinterpret_cast<const uint4*>(gdir + v0));
+        mask = bytes_to_nibble(kind_bytes(kind, f.x, g.x)) |
+               bytes_to_nibble(kind_bytes(kind, f.y, g.y)) << 4 |
+               bytes_to_nibble(kind_bytes(kind, f.z, g.z)) << 8 |
+               bytes_to_nibble(kind_bytes(kind, f.w, g.w)) << 12;
       } else {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          fb[j] = (v0 + j < n) ? fdir[v0 + j] : 0xFF;
-          gb[j] = (v0 + j < n) ? ld<kCoherent>(gdir + v0 + j) : 0xFF;
-        }
+        for (int j = 0; j < 16; ++j)
+          if (v0 + j < n && kind_match(kind, fdir[v0 + j], ld<kCoherent>(gdir + v0 + j)))
+            mask |= 1u << j;
       }
-#pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (kind_match(kind, fb[j], gb[j])) mask |= 1u << j;
     }
     const uint32_t base = warp_reserve(__popc(mask), count);
     uint32_t pos = base;
@@ -442,7 +491,7 @@ __device__ BatchResult small_batch(const State<T>& s, int kind, uint32_t n, uint
 }
 
 template <class T, int DIM>
-__global__ void __launch_bounds__(kSubThreads, 1)
+__global__ void __launch_bounds__(kSubThreads, 2)
     k_subloop(State<T> s, int kind, uint64_t cap, uint32_t batch_base, uint32_t mark_base,
               uint32_t max_batches, uint32_t small_max, uint32_t huge_min) {
   cg::grid_group grid = cg::this_grid();
@@ -579,13 +628,19 @@ struct LabelTile;
 template <>
 struct LabelTile<2> {
   static constexpr int TX = 128, TY = 64, TZ = 1, LX = 7, LY = 6;
+  static constexpr int kSurface = 2 * (TX + TY);
 };
 template <>
 struct LabelTile<3> {
   static constexpr int TX = 32, TY = 16, TZ = 16, LX = 5, LY = 4;
+  static constexpr int kSurface = 2 * (TX * TY + TY * TZ + TX * TZ);
 };
 constexpr int kLabelTileN = 8192;
 constexpr int kLabelTileThreads = 512;
+template <int DIM>
+constexpr size_t label_tile_smem() {
+  return kLabelTileN * 4 + 2 * LabelTile<DIM>::kSurface * 4 + kLabelTileN;
+}
 
 template <int DIM>
 __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
@@ -595,8 +650,17 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
   using TL = LabelTile<DIM>;
   constexpr int NS = StencilSize<DIM>::value;
   constexpr int PER = kLabelTileN / kLabelTileThreads;
-  __shared__ __align__(16) uint8_t sdir[kLabelTileN];
-  __shared__ uint32_t ptr[kLabelTileN];  // (asc local parent) | (desc local parent) << 16
+  // dynamic shared memory (label_tile_smem<DIM>() bytes):
+  //   ptr   u32[kLabelTileN]  (asc local parent) | (desc local parent) << 16
+  //   sexit u32[2][kSurface]  exits can only leave from the tile surface
+  //   sdir  u8[kLabelTileN]
+  extern __shared__ __align__(16) uint8_t label_smem[];
+  uint32_t* ptr = reinterpret_cast<uint32_t*>(label_smem);
+  uint32_t (*sexit)[LabelTile<DIM>::kSurface] =
+      reinterpret_cast<uint32_t (*)[LabelTile<DIM>::kSurface]>(ptr + kLabelTileN);
+  uint8_t* sdir = reinterpret_cast<uint8_t*>(ptr + kLabelTileN + 2 * LabelTile<DIM>::kSurface);
+  __shared__ uint32_t sexit_n[2], sexit_base[2];
+  if (threadIdx.x < 2) sexit_n[threadIdx.x] = 0;
   __shared__ int8_t sd[3][16];
   __shared__ int32_t soff[16];
   if (threadIdx.x < 16) {
@@ -675,16 +739,13 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
     }
     if (!__syncthreads_or(changed)) break;
   }
-  // provisional labels (root, or first vertex outside the tile) + distinct exits
+  // provisional labels (root, or first vertex outside the tile) + the exits
 #pragma unroll
   for (int j = 0; j < PER; ++j) {
     const int i = threadIdx.x + j * kLabelTileThreads;
     const int lx = i & (TL::TX - 1), ly = (i >> TL::LX) & (TL::TY - 1), lz = i >> (TL::LX + TL::LY);
-    const bool val = lx < ex && ly < ey && lz < ez;
-    const uint32_t p = ptr[i];
-    bool fresh[2] = {false, false};
-    uint32_t e[2] = {0, 0};
-    if (val) {
+    if (lx < ex && ly < ey && lz < ez) {
+      const uint32_t p = ptr[i];
       const uint32_t gi = base + lx + g.X * ly + g.XY * lz;
 #pragma unroll
       for (int fam = 0; fam < 2; ++fam) {
@@ -694,38 +755,59 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
                   tlz = t >> (TL::LX + TL::LY);
         const uint32_t res = base + tlx + g.X * tly + g.XY * tlz + soff[c];  // soff[15] = 0
         (fam ? m : M)[gi] = res;
-        if (t == i && c != kSelf) {  // this chain leaves the tile here
-          e[fam] = res;
-          const uint32_t mk = mark_asc + fam;
-          fresh[fam] = __ldcg(mark + res) != mk && atomicExch(mark + res, mk) != mk;
-        }
+        if (t == i && c != kSelf) sexit[fam][atomicAdd(&sexit_n[fam], 1u)] = res;
       }
     }
-    warp_append(fresh[0], e[0], E_asc, counts + 0);
-    warp_append(fresh[1], e[1], E_desc, counts + 1);
   }
+  __syncthreads();
+  if (threadIdx.x < 2 && sexit_n[threadIdx.x])
+    sexit_base[threadIdx.x] = atomicAdd(counts + threadIdx.x, sexit_n[threadIdx.x]);
+  __syncthreads();
+#pragma unroll
+  for (int fam = 0; fam < 2; ++fam) {
+    uint32_t* E = fam ? E_desc : E_asc;
+    for (uint32_t k = threadIdx.x; k < sexit_n[fam]; k += kLabelTileThreads)
+      E[sexit_base[fam] + k] = sexit[fam][k];
+  }
+  (void)mark;
+  (void)mark_asc;
 }
 
+// One doubling round over the unresolved exits: in[] -> out[] keeps only
+// entries whose label is not yet a root (lab[lab[e]] != lab[e]).  cnt[0..1]
+// are the (asc, desc) input sizes, cnt[2..3] the output sizes.  Exits may
+// repeat (no dedupe); concurrent updates of one entry are benign because any
+// value written is an ancestor on the same chain.
 __global__ void __launch_bounds__(256) k_label_exit_jump(uint32_t* __restrict__ M,
                                                          uint32_t* __restrict__ m,
-                                                         const uint32_t* __restrict__ Ea,
-                                                         const uint32_t* __restrict__ Ed,
-                                                         const uint32_t* counts, uint32_t* flag) {
-  const uint32_t na = counts[0], nd = counts[1];
+                                                         const uint32_t* __restrict__ in_a,
+                                                         const uint32_t* __restrict__ in_d,
+                                                         uint32_t* __restrict__ out_a,
+                                                         uint32_t* __restrict__ out_d,
+                                                         const uint32_t* cnt_in, uint32_t* cnt_out) {
+  const uint32_t na = cnt_in[0], nd = cnt_in[1];
+  const uint64_t total = static_cast<uint64_t>(na) + nd;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  bool changed = false;
-  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-       i < static_cast<uint64_t>(na) + nd; i += stride) {
-    uint32_t* lab = i < na ? M : m;
-    const uint32_t e = i < na ? Ea[i] : Ed[i - na];
-    const uint32_t l = lab[e];
-    const uint32_t ll = lab[l];
-    if (ll != l) {
-      lab[e] = ll;
-      changed = true;
+  for (uint64_t wb = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) & ~uint64_t(31);
+       wb < total; wb += stride) {
+    const uint64_t i = wb + (threadIdx.x & 31);
+    bool keep_a = false, keep_d = false;
+    uint32_t e = 0;
+    if (i < total) {
+      const bool asc = i < na;
+      uint32_t* lab = asc ? M : m;
+      e = asc ? in_a[i] : in_d[i - na];
+      const uint32_t l = lab[e];
+      const uint32_t ll = lab[l];
+      if (ll != l) {
+        lab[e] = ll;
+        const uint32_t lll = lab[ll];
+        if (lll != ll) (asc ? keep_a : keep_d) = true;
+      }
     }
+    warp_append(keep_a, e, out_a, cnt_out);
+    warp_append(keep_d, e, out_d, cnt_out + 1);
   }
-  if (__any_sync(0xffffffffu, changed) && (threadIdx.x & 31) == 0) *flag = 1;
 }
 
 __global__ void __launch_bounds__(256) k_label_finish(uint32_t* __restrict__ M,
@@ -812,36 +894,52 @@ __global__ void __launch_bounds__(256) k_rfix(State<T> s, uint32_t batch) {
         }
       }
     }
+    // gather every label first (independent loads in flight), then claim
+    uint32_t ta[4], td[4];
+    bool wa[4], wd[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const uint32_t v = static_cast<uint32_t>(q * 4 + j);
       const uint32_t fc = (fw >> (8 * j)) & 0xFFu, gc = (gw >> (8 * j)) & 0xFFu;
+      wa[j] = (gc & 15u) != (fc & 15u);  // ascending line diverges at v
+      wd[j] = (gc >> 4) != (fc >> 4);    // descending line diverges at v
+      ta[j] = wa[j] ? __ldg(s.gM + v) : 0u;
+      td[j] = wd[j] ? __ldg(s.gm + v) : 0u;
+    }
+    uint32_t fa[4], fd[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t v = static_cast<uint32_t>(q * 4 + j);
+      fa[j] = wa[j] ? __ldg(s.fM + v) : 0u;
+      fd[j] = wd[j] ? __ldg(s.fm + v) : 0u;
+      ta[j] = wa[j] ? __ldg(s.gM + ta[j]) : 0u;
+      td[j] = wd[j] ? __ldg(s.gm + td[j]) : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t v = static_cast<uint32_t>(q * 4 + j);
+      const uint32_t fc = (fw >> (8 * j)) & 0xFFu, gc = (gw >> (8 * j)) & 0xFFu;
+      const bool ma = wa[j] && ta[j] != fa[j];
+      const bool md = wd[j] && td[j] != fd[j];
+      mism += (ma ? 1u : 0u) + (md ? 1u : 0u);
       bool oka = false, okd = false;
-      uint32_t ta = 0, td = 0;
-      if ((gc & 15u) != (fc & 15u)) {  // ascending line diverges at v
-        const uint32_t gl = __ldg(s.gM + v);
-        if (__ldg(s.gM + gl) != __ldg(s.fM + v)) {
-          ++mism;
-          if ((gc & 15u) == kSelf) atomicExch(&s.ctl->status, kStatusTroubleMax);
-          else {
-            ta = v + s.geo.off[gc & 15u];
-            oka = claim_and_lower(s, ta, batch);
-          }
+      uint32_t xa = 0, xd = 0;
+      if (ma) {
+        if ((gc & 15u) == kSelf) atomicExch(&s.ctl->status, kStatusTroubleMax);
+        else {
+          xa = v + s.geo.off[gc & 15u];
+          oka = claim_and_lower(s, xa, batch);
         }
       }
-      if ((gc >> 4) != (fc >> 4)) {  // descending line diverges at v
-        const uint32_t gl = __ldg(s.gm + v);
-        if (__ldg(s.gm + gl) != __ldg(s.fm + v)) {
-          ++mism;
-          if ((fc >> 4) == kSelf) atomicExch(&s.ctl->status, kStatusTroubleMax);
-          else {
-            td = v + s.geo.off[fc >> 4];
-            okd = claim_and_lower(s, td, batch);
-          }
+      if (md) {
+        if ((fc >> 4) == kSelf) atomicExch(&s.ctl->status, kStatusTroubleMax);
+        else {
+          xd = v + s.geo.off[fc >> 4];
+          okd = claim_and_lower(s, xd, batch);
         }
       }
-      warp_append(oka, ta, s.S, &s.ctl->s_count);
-      warp_append(okd, td, s.S, &s.ctl->s_count);
+      warp_append(oka, xa, s.S, &s.ctl->s_count);
+      warp_append(okd, xd, s.S, &s.ctl->s_count);
     }
   }
 #pragma unroll
@@ -854,10 +952,6 @@ __global__ void __launch_bounds__(256) k_rfix(State<T> s, uint32_t batch) {
 // Gate of the R-loop (detect_false_critical().empty(), edit_engine.cpp:338):
 // a vertex is a false critical point of some kind iff its max flag or its min
 // flag differs between f and g.  SWAR over 16 codes per thread.
-__device__ __forceinline__ uint32_t zero_bytes(uint32_t u) {  // 0x80 per zero byte, exact
-  const uint32_t y = (u & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;
-  return ~(y | u | 0x7F7F7F7Fu);
-}
 __device__ __forceinline__ uint32_t false_cp_bytes(uint32_t f, uint32_t g) {
   const uint32_t fmx = zero_bytes(~f & 0x0F0F0F0Fu), gmx = zero_bytes(~g & 0x0F0F0F0Fu);
   const uint32_t fmn = zero_bytes(~f & 0xF0F0F0F0u), gmn = zero_bytes(~g & 0xF0F0F0F0u);
