@@ -1,0 +1,201 @@
+// mssz_b200.hpp — header-only C++ host binding over the C-ABI (mssz_cuda.h)
+// with the reference's proj/core entry-point signatures, so a reference caller
+// (tools/mssz.cpp run_compress / run_fix / run_bench) switches by changing the
+// namespace it calls:
+//
+//   reference:  mssz::derive_edits<T>(topo, f, fhat, xi, opts, &stats)
+//               (/root/reference/proj/core/include/mssz/edit_engine.hpp:183-186)
+//   B200:       mssz_b200::derive_edits<T>(topo, f, fhat, xi, opts, &stats)
+//
+// Types mirror grid.hpp:25-47 (GridTopology), edit_engine.hpp:45-82 (EditSet,
+// EditStats, DeriveOptions), mss.hpp:24-42 (DirectionField, SegmentationLabels)
+// and errors.hpp:9-28 (ErrKind, Error); a nonzero C-ABI return becomes the
+// same mssz_b200::Error{kind} the reference throws.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <functional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "mssz_cuda.h"
+
+namespace mssz_b200 {
+
+using VertexId = std::uint64_t;
+
+enum class ErrKind : int {
+  usage = 2,
+  io = 3,
+  bound_violation = 4,
+  non_convergence = 5,
+  corrupt_archive = 6,
+  internal = 7,
+  cuda = 99,
+};
+
+class Error : public std::runtime_error {
+ public:
+  Error(ErrKind kind, const std::string& msg) : std::runtime_error(msg), kind_(kind) {}
+  ErrKind kind() const noexcept { return kind_; }
+  int exit_code() const noexcept { return static_cast<int>(kind_); }
+
+ private:
+  ErrKind kind_;
+};
+
+inline void check(int rc) {
+  if (rc != 0) throw Error(static_cast<ErrKind>(rc), mssz_cu_last_error());
+}
+
+struct GridTopology {
+  int ndims = 0;
+  std::array<std::uint64_t, 3> dims{1, 1, 1};
+  std::uint64_t vertex_count = 0;
+};
+
+// build_topology (grid.cpp:39-55)
+inline GridTopology build_topology(std::span<const std::uint64_t> dims) {
+  if (dims.size() != 2 && dims.size() != 3)
+    throw Error(ErrKind::usage, "dims must have 2 or 3 extents");
+  GridTopology t;
+  t.ndims = static_cast<int>(dims.size());
+  std::uint64_t count = 1;
+  for (size_t a = 0; a < dims.size(); ++a) {
+    if (dims[a] < 2) throw Error(ErrKind::usage, "every grid extent must be >= 2");
+    if (dims[a] > (std::uint64_t(1) << 40) / count)
+      throw Error(ErrKind::usage, "grid exceeds the address-space cap");
+    t.dims[a] = dims[a];
+    count *= dims[a];
+  }
+  t.vertex_count = count;
+  return t;
+}
+
+template <class T>
+struct EditSet {
+  std::vector<VertexId> indices;
+  std::vector<T> values;
+  std::uint64_t size() const { return indices.size(); }
+  bool empty() const { return indices.empty(); }
+};
+
+struct EditStats : mssz_cu_stats {
+  EditStats() : mssz_cu_stats{} {}
+  std::uint64_t sub_iterations_total() const {
+    return sub_iterations[0] + sub_iterations[1] + sub_iterations[2] + sub_iterations[3];
+  }
+};
+
+template <class T>
+struct DeriveOptions {
+  int device = -1;  // replaces ExecPolicy: which GPU
+  std::uint64_t outer_cap = 1000;
+  std::uint64_t subloop_cap = 640;
+  std::uint64_t r_cap = 100000;
+  bool force = false;
+  std::function<void(std::span<const T>)> on_batch;
+};
+
+struct DirectionField {
+  std::vector<VertexId> asc, desc;
+  bool is_max(VertexId v) const { return asc[v] == v; }
+  bool is_min(VertexId v) const { return desc[v] == v; }
+};
+
+struct SegmentationLabels {
+  std::vector<VertexId> max_label, min_label;
+  bool operator==(const SegmentationLabels&) const = default;
+};
+
+namespace detail {
+template <class T>
+struct Api;
+template <>
+struct Api<float> {
+  static constexpr auto derive = mssz_cu_derive_edits_f32;
+  static constexpr auto directions = mssz_cu_compute_directions_f32;
+  static constexpr auto apply = mssz_cu_apply_edits_f32;
+};
+template <>
+struct Api<double> {
+  static constexpr auto derive = mssz_cu_derive_edits_f64;
+  static constexpr auto directions = mssz_cu_compute_directions_f64;
+  static constexpr auto apply = mssz_cu_apply_edits_f64;
+};
+template <class T>
+void batch_trampoline(const void* g, std::uint64_t n, void* user) {
+  auto* fn = static_cast<std::function<void(std::span<const T>)>*>(user);
+  (*fn)(std::span<const T>(static_cast<const T*>(g), n));
+}
+}  // namespace detail
+
+// derive_edits<T> (edit_engine.hpp:183-186) on the GPU.
+template <class T>
+EditSet<T> derive_edits(const GridTopology& topo, const T* original, const T* decompressed,
+                        double xi, const DeriveOptions<T>& opts = {},
+                        EditStats* stats_out = nullptr) {
+  mssz_cu_options o;
+  mssz_cu_default_options(&o);
+  o.outer_cap = opts.outer_cap;
+  o.subloop_cap = opts.subloop_cap;
+  o.r_cap = opts.r_cap;
+  o.force = opts.force ? 1 : 0;
+  o.device = opts.device;
+  auto cb = opts.on_batch;
+  if (cb) {
+    o.on_batch = &detail::batch_trampoline<T>;
+    o.on_batch_user = &cb;
+  }
+  std::uint64_t* idx = nullptr;
+  T* val = nullptr;
+  std::uint64_t count = 0;
+  EditStats st;
+  check(detail::Api<T>::derive(topo.ndims, topo.dims.data(), original, decompressed, xi, &o,
+                               &idx, &val, &count, &st));
+  EditSet<T> set;
+  set.indices.assign(idx, idx + count);
+  set.values.assign(val, val + count);
+  mssz_cu_free(idx);
+  mssz_cu_free(val);
+  if (stats_out) *stats_out = st;
+  return set;
+}
+
+// compute_directions<T> (mss.hpp:44-50)
+template <class T>
+DirectionField compute_directions(const GridTopology& topo, const T* values) {
+  DirectionField d;
+  d.asc.resize(topo.vertex_count);
+  d.desc.resize(topo.vertex_count);
+  check(detail::Api<T>::directions(topo.ndims, topo.dims.data(), values, d.asc.data(),
+                                   d.desc.data()));
+  return d;
+}
+
+// compute_labels (mss.hpp:58-60)
+inline SegmentationLabels compute_labels(const GridTopology& topo, const DirectionField& d) {
+  SegmentationLabels l;
+  l.max_label.resize(topo.vertex_count);
+  l.min_label.resize(topo.vertex_count);
+  check(mssz_cu_compute_labels(topo.ndims, topo.dims.data(), d.asc.data(), d.desc.data(),
+                               l.max_label.data(), l.min_label.data()));
+  return l;
+}
+
+// apply_edits<T> (edit_engine.hpp:188-190)
+template <class T>
+std::vector<T> apply_edits(const GridTopology& topo, const T* decompressed,
+                           const EditSet<T>& edits) {
+  if (edits.indices.size() != edits.values.size())
+    throw Error(ErrKind::corrupt_archive, "edit set index/value length mismatch");
+  std::vector<T> out(topo.vertex_count);
+  check(detail::Api<T>::apply(topo.vertex_count, decompressed, edits.indices.data(),
+                              edits.values.data(), edits.size(), out.data()));
+  return out;
+}
+
+}  // namespace mssz_b200
