@@ -337,13 +337,13 @@ struct Engine {
       dim3 grid(bx, (geo.Y + chunk - 1) / chunk);
       k_directions_tiled<T, 2><<<grid, DT::BX * DT::BY, 0, ws.stream>>>(vals, dir, geo, chunk);
     } else {
-      using DT = DirTile<3>;
-      const uint32_t bx = (geo.X + DT::BX - 1) / DT::BX, by = (geo.Y + DT::BY - 1) / DT::BY;
+      using DB = DirBlock3<T>;
+      const uint32_t bx = (geo.X + DB::BX - 1) / DB::BX, by = (geo.Y + DB::BY - 1) / DB::BY;
       uint32_t chunk =
           static_cast<uint32_t>(std::max<uint64_t>(4, (uint64_t(geo.Z) * bx * by) / want));
       chunk = std::min<uint32_t>(chunk, 64);
       dim3 grid(bx, by, (geo.Z + chunk - 1) / chunk);
-      k_directions_tiled<T, 3><<<grid, DT::BX * DT::BY, 0, ws.stream>>>(vals, dir, geo, chunk);
+      k_directions_block3<T><<<grid, DB::BX * DB::BY, 0, ws.stream>>>(vals, dir, geo, chunk);
     }
     launched(kProfDirections);
   }
@@ -606,9 +606,8 @@ struct Engine {
       labels_from_codes(s.gdir, lab(2), lab(3), false);
       reset_ctl();
       ws.push_ctl();
-      const uint32_t batch = ws.next_batch++;
       pre(kProfRfix);
-      k_rfix<T><<<grid_for(n(), 256, ws.sms, 16), 256, 0, ws.stream>>>(s, batch);
+      k_rfix<T><<<grid_for(n() / 4 + 1, 256, ws.sms, 16), 256, 0, ws.stream>>>(s, list(0));
       launched(kProfRfix);
       ws.pull_ctl();
       const Ctl c = *ws.hctl;
@@ -616,7 +615,16 @@ struct Engine {
         fail(MSSZ_CU_ERR_INTERNAL, "troublemaker target is an extremum (stale critical report)");
       if (c.mism == 0) return true;
       if (++iters > opt.r_cap) fail(MSSZ_CU_ERR_NON_CONVERGENCE, "R-loop exceeded its iteration cap");
-      const uint32_t applied = c.s_count;
+      // claim each distinct target once and lower it (edit_engine.cpp:344-358)
+      const uint32_t ntargets = c.list_count[0];
+      const uint32_t batch = ws.next_batch++;
+      pre(kProfFix);
+      k_fix_list<T><<<grid_for(ntargets, 256, ws.sms, 16), 256, 0, ws.stream>>>(s, list(0), ntargets,
+                                                                                0, batch);
+      launched(kProfFix);
+      uint32_t applied = 0;
+      CK(cudaMemcpyAsync(&applied, &ws.ctl->s_count, 4, cudaMemcpyDeviceToHost, ws.stream));
+      ws.sync();
       if (applied == 0)
         fail(MSSZ_CU_ERR_NON_CONVERGENCE, "R-loop stalled: every troublemaker is at its floor");
       const uint32_t mark = ws.next_mark++;
@@ -625,9 +633,9 @@ struct Engine {
       } else {
         pre(kProfFrontier);
         if (geo.ndims == 2)
-          k_frontier<T, 2><<<grid_for(applied, 256, ws.sms, 16), 256, 0, ws.stream>>>(s, applied, mark);
+          k_frontier<T, 2><<<grid_for(uint64_t(applied) * 8, 256, ws.sms, 16), 256, 0, ws.stream>>>(s, applied, mark);
         else
-          k_frontier<T, 3><<<grid_for(applied, 256, ws.sms, 16), 256, 0, ws.stream>>>(s, applied, mark);
+          k_frontier<T, 3><<<grid_for(uint64_t(applied) * 16, 256, ws.sms, 16), 256, 0, ws.stream>>>(s, applied, mark);
         launched(kProfFrontier);
       }
       st.effective_edits += applied;
@@ -698,7 +706,7 @@ struct Engine {
       reset_ctl();
       ws.push_ctl();
       pre(kProfRfix);
-      k_rfix<T><<<grid_for(n(), 256, ws.sms, 16), 256, 0, ws.stream>>>(s, ws.next_batch++);
+      k_rfix<T><<<grid_for(n() / 4 + 1, 256, ws.sms, 16), 256, 0, ws.stream>>>(s, list(0));
       launched(kProfRfix);
       ws.pull_ctl();
       if (ws.hctl->mism != 0) fail(MSSZ_CU_ERR_INTERNAL, "converged with mismatched labels");

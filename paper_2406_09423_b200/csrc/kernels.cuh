@@ -165,6 +165,137 @@ __global__ void __launch_bounds__(DirTile<DIM>::BX * DirTile<DIM>::BY)
   }
 }
 
+// K1 (3D, block form).  The 3D Freudenthal link of (x,y,z) plus the vertex
+// itself is exactly the union of four 2x2 cell blocks:
+//   C(z-1) = {x-1,x} x {y-1,y} in plane z-1   slots 13, 9, 11, 5
+//   C(z)   = {x-1,x} x {y-1,y} in plane z     slots  7, 3,  1, SELF
+//   A(z)   = {x,x+1} x {y,y+1} in plane z     slots SELF, 0, 2, 6
+//   A(z+1) = {x,x+1} x {y,y+1} in plane z+1   slots  4, 10, 8, 12
+// whose vertex-index ranges are ordered C(z-1) < C(z) <= A(z) < A(z+1).  So each
+// plane's 2x2 block extremes (with the SoS tie-break inside the block) are
+// computed once per cell and every vertex combines four candidates in that
+// order: >= for ascending (highest index wins ties), < for descending.
+// Out-of-grid cells hold key 0 (and key-1 = ~0 for descending): they never win.
+constexpr uint64_t kBlockSlot3 =  // nibble (candidate * 4 + position) -> stencil slot
+    0xC8A4620FF1375B9Dull;
+
+template <class K>
+struct alignas(sizeof(K) == 4 ? 8 : 16) KeyPos {
+  K key;
+  uint32_t pos;
+};
+
+template <class T>
+struct DirBlock3 {
+  static constexpr int BX = 64, BY = sizeof(T) == 4 ? 8 : 4;
+};
+
+template <class T>
+__global__ void __launch_bounds__(DirBlock3<T>::BX * DirBlock3<T>::BY)
+    k_directions_block3(const T* __restrict__ vals, uint8_t* __restrict__ dir, Geom g, int chunk) {
+  using K = typename KeyOf<T>::type;
+  constexpr int BX = DirBlock3<T>::BX, BY = DirBlock3<T>::BY;
+  constexpr int HX = BX + 2, HY = BY + 2;
+  constexpr int BBX = BX + 1, NB = (BX + 1) * (BY + 1);
+  constexpr int NT = BX * BY;
+  constexpr int PL = (HX * HY + NT - 1) / NT;
+  constexpr int D = 2;
+  __shared__ K stage[HY * HX];
+  __shared__ KeyPos<K> bmx[3][NB];
+  __shared__ KeyPos<K> bmn[3][NB];
+  const int tx = threadIdx.x % BX, ty = threadIdx.x / BX;
+  const int x0 = blockIdx.x * BX, y0 = blockIdx.y * BY;
+  const int S = static_cast<int>(g.Z);
+  const int s0 = blockIdx.z * chunk;
+  const int s1 = min(s0 + chunk, S);
+  int64_t eoff[PL];
+  bool evalid[PL];
+#pragma unroll
+  for (int j = 0; j < PL; ++j) {
+    const int i = threadIdx.x + j * NT;
+    const int hx = i % HX, hy = i / HX;
+    const int x = x0 + hx - 1, y = y0 + hy - 1;
+    evalid[j] = i < HX * HY && x >= 0 && x < static_cast<int>(g.X) && y >= 0 &&
+                y < static_cast<int>(g.Y);
+    eoff[j] = evalid[j] ? static_cast<int64_t>(x) + static_cast<int64_t>(g.X) * y : 0;
+  }
+  const int64_t pstride = static_cast<int64_t>(g.XY);
+  K pre[D][PL];
+  auto fetch = [&](int sp, K* dst) {
+#pragma unroll
+    for (int j = 0; j < PL; ++j)
+      dst[j] = (evalid[j] && sp >= 0 && sp < S) ? okey(__ldg(vals + eoff[j] + pstride * sp)) : K(0);
+  };
+  auto commit = [&](const K* src) {
+#pragma unroll
+    for (int j = 0; j < PL; ++j) {
+      const int i = threadIdx.x + j * NT;
+      if (i < HX * HY) stage[i] = src[j];
+    }
+  };
+  // block extremes of the staged plane into ring slot `slot`
+  auto build = [&](int slot) {
+    for (int b = threadIdx.x; b < NB; b += NT) {
+      const int bx = b % BBX, by = b / BBX;
+      const K c0 = stage[by * HX + bx], c1 = stage[by * HX + bx + 1];
+      const K c2 = stage[(by + 1) * HX + bx], c3 = stage[(by + 1) * HX + bx + 1];
+      K hk = c0, lk = c0 - 1;
+      uint32_t hp = 0, lp = 0;
+      if (c1 >= hk) { hk = c1; hp = 1; }
+      if (c2 >= hk) { hk = c2; hp = 2; }
+      if (c3 >= hk) { hk = c3; hp = 3; }
+      if (c1 - 1 < lk) { lk = c1 - 1; lp = 1; }
+      if (c2 - 1 < lk) { lk = c2 - 1; lp = 2; }
+      if (c3 - 1 < lk) { lk = c3 - 1; lp = 3; }
+      bmx[slot][b] = KeyPos<K>{hk, hp};
+      bmn[slot][b] = KeyPos<K>{lk, lp};
+    }
+  };
+  fetch(s0 - 1, pre[0]);
+  commit(pre[0]);
+  __syncthreads();
+  build((s0 + 2) % 3);
+  __syncthreads();
+  fetch(s0, pre[0]);
+  commit(pre[0]);
+  __syncthreads();
+  build(s0 % 3);
+#pragma unroll
+  for (int u = 0; u < D; ++u) fetch(s0 + 1 + u, pre[u]);
+  const uint32_t x = x0 + tx, y = y0 + ty;
+  const int ci = ty * BBX + tx, ai = (ty + 1) * BBX + tx + 1;
+  for (int sp0 = s0; sp0 < s1; sp0 += D) {
+#pragma unroll
+    for (int u = 0; u < D; ++u) {
+      const int sp = sp0 + u;
+      if (sp >= s1) break;
+      __syncthreads();  // previous build / compute done before the stage is rewritten
+      commit(pre[u]);
+      __syncthreads();
+      fetch(sp + 1 + D, pre[u]);
+      build((sp + 1) % 3);
+      __syncthreads();
+      if (x < g.X && y < g.Y) {
+        const int sm = (sp + 2) % 3, s0_ = sp % 3, sp1 = (sp + 1) % 3;
+        const KeyPos<K> a0 = bmx[sm][ci], a1 = bmx[s0_][ci], a2 = bmx[s0_][ai], a3 = bmx[sp1][ai];
+        const KeyPos<K> d0 = bmn[sm][ci], d1 = bmn[s0_][ci], d2 = bmn[s0_][ai], d3 = bmn[sp1][ai];
+        K hk = a0.key, lk = d0.key;
+        uint32_t hi = a0.pos, lo = d0.pos;
+        if (a1.key >= hk) { hk = a1.key; hi = 4 + a1.pos; }
+        if (a2.key >= hk) { hk = a2.key; hi = 8 + a2.pos; }
+        if (a3.key >= hk) { hk = a3.key; hi = 12 + a3.pos; }
+        if (d1.key < lk) { lk = d1.key; lo = 4 + d1.pos; }
+        if (d2.key < lk) { lk = d2.key; lo = 8 + d2.pos; }
+        if (d3.key < lk) { lk = d3.key; lo = 12 + d3.pos; }
+        const uint32_t hc = static_cast<uint32_t>(kBlockSlot3 >> (4 * hi)) & 15u;
+        const uint32_t lc = static_cast<uint32_t>(kBlockSlot3 >> (4 * lo)) & 15u;
+        dir[static_cast<uint64_t>(x) + static_cast<uint64_t>(g.X) * y +
+            static_cast<uint64_t>(g.XY) * sp] = static_cast<uint8_t>(hc | (lc << 4));
+      }
+    }
+  }
+}
+
 // K1b (k_detect_kind, the full detect sweep) is defined with the subloop helpers below.
 
 // Counts of the first-match classes (detect_false_critical, edit_engine.cpp:134-158)
@@ -271,43 +402,57 @@ __device__ __forceinline__ void fix_batch(const State<T>& s, const uint32_t* __r
   }
 }
 
+// Stencil slot k -> (dx, dy, dz) without tables: slots come in (+d, -d) pairs
+// (grid.cpp:8-16); pair j's components are bit j of a per-axis mask.
+template <int DIM>
+__device__ __forceinline__ void slot_delta(int k, int& dx, int& dy, int& dz) {
+  const int j = k >> 1, sgn = (k & 1) ? -1 : 1;
+  if (DIM == 2) {
+    dx = ((0x5 >> j) & 1) * sgn;
+    dy = ((0x6 >> j) & 1) * sgn;
+    dz = 0;
+  } else {
+    dx = ((0x69 >> j) & 1) * sgn;
+    dy = ((0x5A >> j) & 1) * sgn;
+    dz = ((0x74 >> j) & 1) * sgn;
+  }
+}
+
 // Re-evaluates gdir on S ∪ N(S) (the only vertices whose direction can change
 // after a batch), each vertex once (fmark dedupe), and collects them in F.
+// One lane per (edited vertex, candidate slot): 16 lanes per vertex in 3D
+// (self + 14 slots), 8 in 2D, so every lane has one claim and one direction
+// evaluation in flight instead of a serial chain of 15.
 template <class T, int DIM>
 __device__ __forceinline__ void frontier_update(const State<T>& s, uint32_t ns, uint32_t mark,
                                                 uint32_t* f_count, uint64_t tid, uint64_t stride) {
+  constexpr int LPS = DIM == 2 ? 8 : 16;  // lanes per edited vertex
   constexpr int NS = StencilSize<DIM>::value;
-  for (uint64_t wb = tid & ~uint64_t(31); wb < ns; wb += stride) {
+  const uint64_t total = static_cast<uint64_t>(ns) * LPS;
+  for (uint64_t wb = tid & ~uint64_t(31); wb < total; wb += stride) {
     const uint64_t i = wb + (threadIdx.x & 31);
-    uint32_t sv = 0, sx = 0, sy = 0, sz = 0;
-    const bool live = i < ns;
-    if (live) {
-      sv = __ldcg(s.S + i);
-      coords(s.geo, sv, sx, sy, sz);
-    }
-#pragma unroll
-    for (int k = -1; k < NS; ++k) {
-      bool mine = false;
-      uint32_t u = sv;
-      if (live) {
-        uint32_t ux = sx, uy = sy, uz = sz;
-        bool valid = true;
-        if (k >= 0) {
-          valid = in_grid<DIM>(s.geo, sx, sy, sz, k);
-          int dx, dy, dz;
-          stencil<DIM>(k, dx, dy, dz);
-          ux = sx + dx;
-          uy = sy + dy;
-          uz = sz + dz;
-          u = sv + slot_offset<DIM>(s.geo, k);
-        }
-        if (valid && __ldcg(s.fmark + u) != mark && atomicExch(&s.fmark[u], mark) != mark) {
-          mine = true;
-          s.gdir[u] = static_cast<uint8_t>(direction_code<T, DIM, true>(s.g, s.geo, u, ux, uy, uz));
+    bool mine = false;
+    uint32_t u = 0;
+    if (i < total) {
+      const int k = static_cast<int>(i % LPS) - 1;  // -1 = the edited vertex itself
+      if (k < NS) {
+        const uint32_t sv = __ldcg(s.S + i / LPS);
+        uint32_t x, y, z;
+        coords(s.geo, sv, x, y, z);
+        int dx = 0, dy = 0, dz = 0;
+        if (k >= 0) slot_delta<DIM>(k, dx, dy, dz);
+        const uint32_t ux = x + dx, uy = y + dy, uz = z + dz;
+        if (ux < s.geo.X && uy < s.geo.Y && (DIM == 2 || uz < s.geo.Z)) {
+          u = ux + s.geo.X * uy + s.geo.XY * uz;
+          if (__ldcg(s.fmark + u) != mark && atomicExch(&s.fmark[u], mark) != mark) {
+            mine = true;
+            s.gdir[u] =
+                static_cast<uint8_t>(direction_code<T, DIM, true>(s.g, s.geo, u, ux, uy, uz));
+          }
         }
       }
-      warp_append(mine, u, s.F, f_count);
     }
+    warp_append(mine, u, s.F, f_count);
   }
 }
 
@@ -862,7 +1007,9 @@ __global__ void k_u32_to_u64(const uint32_t* __restrict__ in, uint64_t* __restri
 //   { fdesc(w) : gdesc(w) != fdesc(w), gm(w) != fm(w) }
 // and one full sweep finds it without walking.  Targets are claimed once and
 // lowered from the pre-batch g, which is the reference's batch semantics (claim
-// stamps, then lower_step over the deduplicated targets).
+// stamps, then lower_step over the deduplicated targets).  k_rfix only lists
+// the targets (a streaming pass with no atomics on its critical path);
+// k_fix_list then claims and lowers them.
 //
 // The g labels arrive provisional (k_label_tile + exit jumping, no finish
 // pass): lab[v] is a root or a resolved exit, so lab[lab[v]] is final.  Only
@@ -871,7 +1018,7 @@ __global__ void k_u32_to_u64(const uint32_t* __restrict__ in, uint64_t* __restri
 // vertex is mismatched (the walk argument above), which is the reference's
 // collect_mismatched() == 0 test.
 template <class T>
-__global__ void __launch_bounds__(256) k_rfix(State<T> s, uint32_t batch) {
+__global__ void __launch_bounds__(256) k_rfix(State<T> s, uint32_t* __restrict__ targets) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   uint32_t mism = 0;
@@ -928,18 +1075,19 @@ __global__ void __launch_bounds__(256) k_rfix(State<T> s, uint32_t batch) {
         if ((gc & 15u) == kSelf) atomicExch(&s.ctl->status, kStatusTroubleMax);
         else {
           xa = v + s.geo.off[gc & 15u];
-          oka = claim_and_lower(s, xa, batch);
+          oka = true;
         }
       }
       if (md) {
         if ((fc >> 4) == kSelf) atomicExch(&s.ctl->status, kStatusTroubleMax);
         else {
           xd = v + s.geo.off[fc >> 4];
-          okd = claim_and_lower(s, xd, batch);
+          okd = true;
         }
       }
-      warp_append(oka, xa, s.S, &s.ctl->s_count);
-      warp_append(okd, xd, s.S, &s.ctl->s_count);
+      // targets only; claims + lowering run afterwards in k_fix_list (rule self)
+      warp_append(oka, xa, targets, &s.ctl->list_count[0]);
+      warp_append(okd, xd, targets, &s.ctl->list_count[0]);
     }
   }
 #pragma unroll
