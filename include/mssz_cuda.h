@@ -88,6 +88,7 @@ typedef struct mssz_cu_options {
 #define MSSZ_CU_PROF_COMPACT 9
 #define MSSZ_CU_PROF_LABEL_FINISH 10
 #define MSSZ_CU_PROF_FIX 11 /* host-driven huge batch: fix_list */
+#define MSSZ_CU_PROF_SPARSE 12 /* sparse R iteration kernels */
 #define MSSZ_CU_PROF_CLASSES 16
 
 /* Mirrors EditStats (edit_engine.hpp:54-68) field for field, then adds the
@@ -113,6 +114,10 @@ typedef struct mssz_cu_stats {
   uint64_t kernel_launches;   /* kernels launched by this call */
   uint64_t big_batches;       /* C batches run grid-wide inside the persistent kernel */
   uint64_t huge_batches;      /* C batches run by host-launched streaming kernels */
+  uint64_t label_tiles;       /* label tiles re-resolved (phase 1) over all label passes */
+  uint64_t rfix_tiles;        /* label tiles whose mismatch bits were recomputed */
+  uint64_t sparse_iterations; /* R iterations resolved by the sparse Up(X) pass */
+  uint64_t sparse_up;         /* sum of |Up(X)| over sparse passes */
   uint64_t kernel_count[MSSZ_CU_PROF_CLASSES]; /* launches per kernel class */
   double kernel_ms[MSSZ_CU_PROF_CLASSES];      /* device ms per class (profile = 1 only) */
 } mssz_cu_stats;

@@ -147,6 +147,10 @@ class EditStats:
     kernel_launches: int = 0
     big_batches: int = 0
     huge_batches: int = 0
+    label_tiles: int = 0
+    rfix_tiles: int = 0
+    sparse_iterations: int = 0
+    sparse_up: int = 0
     kernel_count: list = field(default_factory=lambda: [0] * 16)
     kernel_ms: list = field(default_factory=lambda: [0.0] * 16)
 
@@ -243,7 +247,8 @@ class _Stats(C.Structure):
         ("label_passes", C.c_uint64), ("label_rounds", C.c_uint64),
         ("detect_sweeps", C.c_uint64), ("frontier_vertices", C.c_uint64),
         ("kernel_launches", C.c_uint64), ("big_batches", C.c_uint64),
-        ("huge_batches", C.c_uint64),
+        ("huge_batches", C.c_uint64), ("label_tiles", C.c_uint64), ("rfix_tiles", C.c_uint64),
+        ("sparse_iterations", C.c_uint64), ("sparse_up", C.c_uint64),
         ("kernel_count", C.c_uint64 * 16), ("kernel_ms", C.c_double * 16),
     ]
 
@@ -256,7 +261,7 @@ class _Stats(C.Structure):
 
 _ARRAY_FIELDS = ("sub_iterations", "kernel_count", "kernel_ms")
 PROF_CLASSES = ["validate", "directions", "detect_kind", "detect_all", "subloop", "label_init",
-                "label_jump", "rfix", "frontier", "compact", "label_finish", "fix"]
+                "label_jump", "rfix", "frontier", "compact", "label_finish", "fix", "sparse"]
 
 
 _BATCH_CB = C.CFUNCTYPE(None, C.c_void_p, C.c_uint64, C.c_void_p)

@@ -81,11 +81,14 @@ struct KeyOf<double> {
   using type = uint64_t;
 };
 
-// Loads: LDG for data that is constant during the launch, L2-only (.cg) for
-// data other CTAs of the same persistent launch may have written.
+// Loads: LDG (read-only path) for data that is constant during the launch;
+// plain (weak, L1-cacheable) loads for data other CTAs of the same persistent
+// launch wrote before the last grid/block barrier -- the barrier's gpu-scope
+// fence orders those writes before these loads (and invalidates L1), so the
+// 16 lanes re-reading one edited vertex's neighbourhood can hit in L1.
 template <bool kCoherent, class T>
 __device__ __forceinline__ T ld(const T* p) {
-  if constexpr (kCoherent) return __ldcg(p);
+  if constexpr (kCoherent) return *p;
   else return __ldg(p);
 }
 
@@ -232,6 +235,21 @@ __device__ __forceinline__ void warp_append(bool pred, uint32_t val, uint32_t* _
   if (lane == leader) base = atomicAdd(count, static_cast<uint32_t>(__popc(b)));
   base = __shfl_sync(0xffffffffu, base, leader);
   if (pred) list[base + __popc(b & ((1u << lane) - 1u))] = val;
+}
+
+// warp_append variant that drops entries past `cap` (the count still grows,
+// so the caller detects the overflow).
+__device__ __forceinline__ void warp_append_cap(bool pred, uint32_t val, uint32_t* __restrict__ list,
+                                                uint32_t* count, uint32_t cap) {
+  const unsigned b = __ballot_sync(0xffffffffu, pred);
+  if (b == 0) return;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(b) - 1;
+  uint32_t base = 0;
+  if (lane == leader) base = atomicAdd(count, static_cast<uint32_t>(__popc(b)));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  const uint32_t pos = base + __popc(b & ((1u << lane) - 1u));
+  if (pred && pos < cap) list[pos] = val;
 }
 
 // Per-lane count c -> returns this lane's slot base after a single warp atomic.

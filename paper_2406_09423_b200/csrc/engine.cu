@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -145,7 +146,10 @@ struct Workspace {
   int device = 0;
   int sms = 0;
   cudaStream_t stream = nullptr;
-  DevBuf f, g, fdir, gdir, touched, stamp, fmark, lab, lists, tiles;
+  DevBuf f, g, fdir, gdir, touched, stamp, fmark, lab, fin, lists, tiles;
+  DevBuf tE, tEcnt, toldfin, tdirty, taffected, tbits, tcnt, tlist;  // label-tile store
+  DevBuf xbuf;  // sparse R pass: crossing lists X (2 families x 2 buffers)
+  DevBuf cbits; // 1 bit per 64-vertex chunk whose direction codes changed
   Ctl* ctl = nullptr;
   Ctl* hctl = nullptr;  // pinned mirror
   uint32_t next_batch = 1, next_mark = 1;
@@ -176,7 +180,8 @@ struct Workspace {
                             static_cast<int>(label_tile_smem<3>())));
   }
   void release() {
-    for (DevBuf* b : {&f, &g, &fdir, &gdir, &touched, &stamp, &fmark, &lab, &lists, &tiles})
+    for (DevBuf* b : {&f, &g, &fdir, &gdir, &touched, &stamp, &fmark, &lab, &fin, &lists, &tiles,
+                      &tE, &tEcnt, &toldfin, &tdirty, &taffected, &tbits, &tcnt, &tlist, &xbuf, &cbits})
       b->release();
     next_batch = next_mark = 1;
   }
@@ -192,6 +197,8 @@ struct Workspace {
     bool fresh = stamp.ensure(np * 4);
     fresh |= fmark.ensure(np * 4);
     lab.ensure(np * 16);    // fM fm gM gm (u32)
+    fin.ensure(np * 8);     // exit finals (finM finm), see k_exit_*
+    cbits.ensure((n + 2047) / 2048 * 4 + 4);
     lists.ensure(np * 16);  // list0 list1 S F (u32); reused as the u64+T EditSet
     tiles.ensure(((n + kCompactTile - 1) / kCompactTile + 1) * 4);
     if (fresh || next_batch > 0xF0000000u || next_mark > 0xF0000000u) {
@@ -199,6 +206,18 @@ struct Workspace {
       CK(cudaMemsetAsync(fmark.p, 0, fmark.cap, stream));
       next_batch = next_mark = 1;
     }
+  }
+
+  // label-tile store for ntiles tiles of the given surface
+  void ensure_tiles(uint32_t ntiles, uint32_t surface) {
+    tE.ensure(size_t(ntiles) * 2 * surface * 4);
+    toldfin.ensure(size_t(ntiles) * 2 * surface * 4);
+    tEcnt.ensure(size_t(ntiles) * 2 * 4);
+    tdirty.ensure(ntiles);
+    taffected.ensure(ntiles);
+    tbits.ensure(size_t(ntiles) * 2 * (kLabelTileN / 32) * 4);
+    tcnt.ensure(size_t(ntiles) * 4);
+    tlist.ensure(size_t(ntiles) * 3 * 4 + 16);
   }
 
   void push_ctl() { CK(cudaMemcpyAsync(ctl, hctl, sizeof(Ctl), cudaMemcpyHostToDevice, stream)); }
@@ -235,6 +254,11 @@ Workspace& workspace(int device) {
 constexpr uint32_t kSmallBatchMax = 4096;
 // worklists above n / kHugeBatchDivisor are run by host-launched streaming kernels
 uint32_t kHugeBatchDivisor = 64;  // tunable via MSSZ_HUGE_DIVISOR (experiments)
+// R iterations after one with fewer than n / kSparseMismDivisor mismatches use the
+// sparse pass; it gives up when Up(X) exceeds n / kSparseUpDivisor vertices
+uint32_t kSparseMismDivisor = 1024;
+uint32_t kSparseUpDivisor = 16;
+uint32_t kSparseMaxLevels = 256;  // deeper upstream trees go to the full pass
 
 const char* kKindName[4] = {"FPmax", "FPmin", "FNmax", "FNmin"};
 
@@ -252,6 +276,7 @@ enum {
   kProfCompact = MSSZ_CU_PROF_COMPACT,
   kProfLabelFinish = MSSZ_CU_PROF_LABEL_FINISH,
   kProfFix = MSSZ_CU_PROF_FIX,
+  kProfSparse = MSSZ_CU_PROF_SPARSE,
 };
 
 // ---------------------------------------------------------------------------
@@ -265,6 +290,12 @@ struct Engine {
   uint32_t cur = 0;
   int coop_blocks = 0;
   std::vector<T> host_g;  // on_batch snapshots only
+  bool trace = std::getenv("MSSZ_TRACE") != nullptr;  // per-iteration log on stderr
+  uint64_t r_last_mism = ~uint64_t(0);  // mismatches of the latest R iteration
+  bool r_full_valid = false;            // tile label state matches gdir (no C edits since)
+  bool x_valid = false;                 // crossing lists X match gdir (for k_cross_update)
+  int x_cur[2] = {0, 0};
+  uint32_t x_n[2] = {0, 0};
   size_t prof_n = 0;
   std::vector<int> prof_cls;
   float dir_ms = 0.f, lab_ms = 0.f;
@@ -273,6 +304,7 @@ struct Engine {
 
   uint32_t n() const { return geo.n; }
   uint32_t* list(int k) const { return ws.lists.as<uint32_t>() + static_cast<uint64_t>(k) * ((n() + 63) & ~63u); }
+  uint32_t* list_ptr(int k) const { return list(k); }
   uint32_t* lab(int k) const { return ws.lab.as<uint32_t>() + static_cast<uint64_t>(k) * ((n() + 63) & ~63u); }
 
   void bind(const T* d_f) {
@@ -294,6 +326,8 @@ struct Engine {
     s.gm = lab(3);
     s.xi = 0;
     s.ctl = ws.ctl;
+    s.tdirty = nullptr;
+    s.cdirty = ws.cbits.as<uint32_t>();
   }
 
   // Per-kernel-class device time (CUDA events on the launching stream), only
@@ -327,6 +361,8 @@ struct Engine {
 
   // K1 full sweep: 2.5D smem-tiled, chunk of the streamed axis sized for >= 8 CTAs/SM.
   void directions(const T* vals, uint8_t* dir) {
+    if (dir == s.gdir && s.cdirty)  // every code may change: X must re-evaluate all chunks
+      CK(cudaMemsetAsync(s.cdirty, 0xFF, (n() + 2047) / 2048 * 4, ws.stream));
     pre(kProfDirections);
     const uint64_t want = static_cast<uint64_t>(ws.sms) * 8;
     if (geo.ndims == 2) {
@@ -377,46 +413,105 @@ struct Engine {
   }
 
   // Tiled labels (k_label_tile -> exit jumping -> k_label_finish).
-  // finish = false leaves provisional labels (root or resolved exit): lab[lab[v]] is final.
-  void labels_from_codes(const uint8_t* dir, uint32_t* M, uint32_t* m, bool finish) {
-    CK(cudaEventRecord(ws.ev[2], ws.stream));
-    CK(cudaMemsetAsync(&ws.ctl->s_count, 0, 2 * sizeof(uint32_t), ws.stream));
-    const uint32_t mark_asc = ws.next_mark;
-    ws.next_mark += 2;
-    uint64_t ntiles;
-    pre(kProfLabelInit);
+  uint32_t label_tiles() const {
     if (geo.ndims == 2) {
       using TL = LabelTile<2>;
-      ntiles = uint64_t((geo.X + TL::TX - 1) / TL::TX) * ((geo.Y + TL::TY - 1) / TL::TY);
-      k_label_tile<2><<<static_cast<uint32_t>(ntiles), kLabelTileThreads, label_tile_smem<2>(),
-                        ws.stream>>>(
-          dir, geo, M, m, s.fmark, mark_asc, list(2), list(3), &ws.ctl->s_count);
-    } else {
-      using TL = LabelTile<3>;
-      ntiles = uint64_t((geo.X + TL::TX - 1) / TL::TX) * ((geo.Y + TL::TY - 1) / TL::TY) *
-               ((geo.Z + TL::TZ - 1) / TL::TZ);
-      k_label_tile<3><<<static_cast<uint32_t>(ntiles), kLabelTileThreads, label_tile_smem<3>(),
-                        ws.stream>>>(
-          dir, geo, M, m, s.fmark, mark_asc, list(2), list(3), &ws.ctl->s_count);
+      return ((geo.X + TL::TX - 1) / TL::TX) * ((geo.Y + TL::TY - 1) / TL::TY);
     }
-    launched(kProfLabelInit);
-    // exit chains cross at most ntiles tiles: doubling needs <= bit_width(ntiles)+1
-    // rounds.  Rounds are launched blind (no host sync); each compacts the
-    // unresolved exits into the other list pair, so late rounds are near-empty.
-    const int rounds = bit_width_u64(ntiles) + 2;
-    const uint32_t blocks = grid_for(n() / 8 + 1, 256, ws.sms, 16);
+    using TL = LabelTile<3>;
+    return ((geo.X + TL::TX - 1) / TL::TX) * ((geo.Y + TL::TY - 1) / TL::TY) *
+           ((geo.Z + TL::TZ - 1) / TL::TZ);
+  }
+
+  TileStore tile_store() {
+    TileStore t{};
+    t.ntiles = label_tiles();
+    t.surface = geo.ndims == 2 ? LabelTile<2>::kSurface : LabelTile<3>::kSurface;
+    ws.ensure_tiles(t.ntiles, t.surface);
+    t.E = ws.tE.as<uint32_t>();
+    t.Ecnt = ws.tEcnt.as<uint32_t>();
+    t.oldfin = ws.toldfin.as<uint32_t>();
+    t.dirty = ws.tdirty.as<uint8_t>();
+    t.affected = ws.taffected.as<uint8_t>();
+    t.mis_bits = ws.tbits.as<uint32_t>();
+    t.mis_cnt = ws.tcnt.as<uint32_t>();
+    return t;
+  }
+  uint32_t* tile_list(int k) const { return ws.tlist.as<uint32_t>() + size_t(k) * label_tiles(); }
+  uint32_t* fin(int k) const { return ws.fin.as<uint32_t>() + size_t(k) * ((n() + 63) & ~63u); }
+
+  // tiles selected by k_select_tiles(mode) into tile_list(slot); returns the count
+  uint32_t select_tiles(const TileStore& ts, int mode, int slot) {
+    CK(cudaMemsetAsync(&ws.ctl->cmd_n, 0, sizeof(uint32_t), ws.stream));
+    k_select_tiles<<<grid_for(ts.ntiles, 256, ws.sms, 8), 256, 0, ws.stream>>>(ts, mode, tile_list(slot),
+                                                                             &ws.ctl->cmd_n);
+    CK_LAUNCH();
+    uint32_t c = 0;
+    CK(cudaMemcpyAsync(&c, &ws.ctl->cmd_n, 4, cudaMemcpyDeviceToHost, ws.stream));
+    ws.sync();
+    return c;
+  }
+
+  // Tiled labels: phase 1 on all tiles (or only dirty ones), phase 2 over every
+  // tile's exits with change detection (-> ts.affected), optional phase 3.
+  // Afterwards fin[prov[v]] is v's final label; with finish, prov[v] is final.
+  void label_pass(const uint8_t* dir, uint32_t* M, uint32_t* m, bool only_dirty, bool finish) {
+    CK(cudaEventRecord(ws.ev[2], ws.stream));
+    TileStore ts = tile_store();
+    uint32_t* fM = fin(0);
+    uint32_t* fm = fin(1);
+    uint32_t ntodo = ts.ntiles;
+    const uint32_t* list = nullptr;
+    if (only_dirty) {
+      ntodo = select_tiles(ts, 0, 0);
+      list = tile_list(0);
+    }
+    if (ntodo) {
+      pre(kProfLabelInit);
+      if (geo.ndims == 2)
+        k_label_tile<2><<<ntodo, kLabelTileThreads, label_tile_smem<2>(), ws.stream>>>(
+            dir, geo, M, m, fM, fm, list, ts);
+      else
+        k_label_tile<3><<<ntodo, kLabelTileThreads, label_tile_smem<3>(), ws.stream>>>(
+            dir, geo, M, m, fM, fm, list, ts);
+      launched(kProfLabelInit);
+    }
+    st.label_tiles += ntodo;
+    // phase 2: exits restart from their provisional label, then doubling.  Exit
+    // chains cross at most ntiles tiles: <= bit_width(ntiles)+1 rounds, launched
+    // blind (no host sync); each round compacts the unresolved exits.
+    if (only_dirty) {  // old finals only matter for change detection
+      pre(kProfLabelJump);
+      k_exit_save<<<ts.ntiles, 256, 0, ws.stream>>>(ts, fM, fm);
+      launched(kProfLabelJump);
+    }
+    pre(kProfLabelJump);
+    k_exit_reset<<<ts.ntiles, 256, 0, ws.stream>>>(ts, M, m, fM, fm);
+    launched(kProfLabelJump);
     uint32_t* cnt[2] = {&ws.ctl->s_count, &ws.ctl->list_count[0]};  // (asc, desc) pairs
-    uint32_t* la[2] = {list(2), list(0)};
-    uint32_t* ld[2] = {list(3), list(1)};
+    uint32_t* la[2] = {list_ptr(2), list_ptr(0)};
+    uint32_t* ld[2] = {list_ptr(3), list_ptr(1)};
+    CK(cudaMemsetAsync(cnt[0], 0, 2 * sizeof(uint32_t), ws.stream));
+    pre(kProfLabelJump);
+    k_exit_jump_tiles<<<ts.ntiles, 256, 0, ws.stream>>>(ts, fM, fm, la[0], ld[0], cnt[0]);
+    launched(kProfLabelJump);
+    const int rounds = bit_width_u64(ts.ntiles) + 1;
+    const uint32_t blocks = grid_for(n() / 8 + 1, 256, ws.sms, 16);
     for (int r = 0; r < rounds; ++r) {
       const int a = r & 1, b2 = a ^ 1;
       CK(cudaMemsetAsync(cnt[b2], 0, 2 * sizeof(uint32_t), ws.stream));
       pre(kProfLabelJump);
-      k_label_exit_jump<<<blocks, 256, 0, ws.stream>>>(M, m, la[a], ld[a], la[b2], ld[b2], cnt[a],
+      k_label_exit_jump<<<blocks, 256, 0, ws.stream>>>(fM, fm, la[a], ld[a], la[b2], ld[b2], cnt[a],
                                                       cnt[b2]);
       launched(kProfLabelJump);
     }
-    st.label_rounds += rounds;
+    st.label_rounds += rounds + 1;
+    CK(cudaMemsetAsync(ts.affected, 0, ts.ntiles, ws.stream));
+    if (only_dirty) {
+      pre(kProfLabelJump);
+      k_exit_changed<<<ts.ntiles, 256, 0, ws.stream>>>(ts, fM, fm);
+      launched(kProfLabelJump);
+    }
     uint32_t left[2];
     CK(cudaMemcpyAsync(left, cnt[rounds & 1], sizeof left, cudaMemcpyDeviceToHost, ws.stream));
     ws.sync();
@@ -424,7 +519,7 @@ struct Engine {
       fail(MSSZ_CU_ERR_INTERNAL, "path compression exceeded its round cap (corrupt direction field)");
     if (finish) {
       pre(kProfLabelFinish);
-      k_label_finish<<<grid_for(n() / 4 + 1, 256, ws.sms, 16), 256, 0, ws.stream>>>(M, m, n());
+      k_label_finish<<<grid_for(n() / 4 + 1, 256, ws.sms, 16), 256, 0, ws.stream>>>(M, m, fM, fm, n());
       launched(kProfLabelFinish);
     }
     CK(cudaEventRecord(ws.ev[3], ws.stream));
@@ -435,6 +530,45 @@ struct Engine {
     ++st.label_passes;
   }
 
+  // R batch targets from the tile mismatch bitmaps (k_rfix_tiles on the given
+  // tiles first); returns the total mismatch count, targets in list(0).
+  uint64_t r_targets(bool all_tiles) {
+    TileStore ts = tile_store();
+    uint32_t nt = ts.ntiles;
+    const uint32_t* list = nullptr;
+    if (!all_tiles) {
+      nt = select_tiles(ts, 1, 1);  // dirty or affected
+      list = tile_list(1);
+    }
+    reset_ctl();
+    ws.push_ctl();
+    if (nt) {
+      pre(kProfRfix);
+      if (geo.ndims == 2)
+        k_rfix_tiles<T, 2><<<nt, 256, 0, ws.stream>>>(s, list, ts, fin(0), fin(1));
+      else
+        k_rfix_tiles<T, 3><<<nt, 256, 0, ws.stream>>>(s, list, ts, fin(0), fin(1));
+      launched(kProfRfix);
+    }
+    st.rfix_tiles += nt;
+    const uint32_t nm = select_tiles(ts, 2, 2);  // tiles with mismatches
+    if (nm) {
+      pre(kProfRfix);
+      if (geo.ndims == 2)
+        k_expand_targets<T, 2><<<nm, 256, 0, ws.stream>>>(s, tile_list(2), ts, list_ptr(0),
+                                                          &ws.ctl->list_count[0]);
+      else
+        k_expand_targets<T, 3><<<nm, 256, 0, ws.stream>>>(s, tile_list(2), ts, list_ptr(0),
+                                                          &ws.ctl->list_count[0]);
+      launched(kProfRfix);
+    }
+    CK(cudaMemsetAsync(ts.dirty, 0, ts.ntiles, ws.stream));
+    ws.pull_ctl();
+    if (ws.hctl->status == kStatusTroubleMax)
+      fail(MSSZ_CU_ERR_INTERNAL, "troublemaker target is an extremum (stale critical report)");
+    return ws.hctl->mism;
+  }
+
   void reset_ctl() {
     std::memset(ws.hctl, 0, sizeof(Ctl));
     ws.hctl->cur = cur;
@@ -443,6 +577,7 @@ struct Engine {
   int coop_grid() {
     if (coop_blocks) return coop_blocks;
     if (const char* h = std::getenv("MSSZ_HUGE_DIVISOR")) kHugeBatchDivisor = std::max(1, std::atoi(h));
+    if (const char* h = std::getenv("MSSZ_SPARSE_DIVISOR")) kSparseMismDivisor = std::max(1, std::atoi(h));
     int occ = 0;
     if (geo.ndims == 2)
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subloop<T, 2>, kSubThreads, 0));
@@ -567,6 +702,10 @@ struct Engine {
       fail(MSSZ_CU_ERR_NON_CONVERGENCE, "%s subloop exceeded its iteration cap", kKindName[kind]);
     if (c.status == kStatusStall)
       fail(MSSZ_CU_ERR_NON_CONVERGENCE, "%s subloop stalled at the float floor", kKindName[kind]);
+    if (trace)
+      std::fprintf(stderr, "[mssz] C kind=%d iters=%llu edits=%llu big=%llu frontier=%llu\n", kind,
+                   (unsigned long long)c.iters, (unsigned long long)c.edits,
+                   (unsigned long long)c.big_batches, (unsigned long long)c.frontier);
     st.sub_iterations[kind] += c.iters;
     st.effective_edits += c.edits;
     st.frontier_vertices += c.frontier;
@@ -580,15 +719,22 @@ struct Engine {
       ++st.c_passes;
       uint64_t pass_edits = 0;
       for (int kind = 0; kind < 4; ++kind) pass_edits += run_subloop(kind);
+      if (pass_edits) r_full_valid = false;  // the tile store no longer matches gdir
       if (pass_edits == 0) return;
     }
   }
 
-  uint64_t count_false_critical() {
+  // frontier_only: count over the F list of the last k_frontier (its vertices
+  // are the only ones whose codes changed since a state with no false CPs)
+  uint64_t count_false_critical(bool frontier_only = false) {
     CK(cudaMemsetAsync(&ws.ctl->counts[0], 0, sizeof(uint64_t), ws.stream));
     pre(kProfDetectAll);
-    k_count_false<<<grid_for(n() / 16 + 1, 256, ws.sms, 16), 256, 0, ws.stream>>>(
-        s.fdir, s.gdir, n(), &ws.ctl->counts[0]);
+    if (frontier_only)
+      k_count_false_list<<<grid_for(n() / 64 + 1, 256, ws.sms, 8), 256, 0, ws.stream>>>(
+          s.fdir, s.gdir, s.F, &ws.ctl->f_count, &ws.ctl->counts[0]);
+    else
+      k_count_false<<<grid_for(n() / 16 + 1, 256, ws.sms, 16), 256, 0, ws.stream>>>(
+          s.fdir, s.gdir, n(), &ws.ctl->counts[0]);
     launched(kProfDetectAll);
     ++st.detect_sweeps;
     uint64_t total = 0;
@@ -599,25 +745,178 @@ struct Engine {
 
   // run_r_loop (edit_engine.cpp:329-366).  Returns true when it stopped on
   // matching labels (the outer loop's postcondition), false on new false CPs.
+  // Sparse R batch targets (k_cross -> k_upstream -> restricted jumping ->
+  // k_up_targets, see kernels.cuh).  Returns false (nothing emitted) when
+  // Up(X) grows past max_up, in which case the caller runs the full pass.
+  uint32_t x_cap() const { return std::max<uint32_t>(1u << 16, n() / kSparseUpDivisor); }
+  uint32_t* xlist(int fam, int k) {
+    ws.xbuf.ensure(size_t(x_cap()) * 4 * 4);
+    return ws.xbuf.as<uint32_t>() + size_t(fam * 2 + k) * x_cap();
+  }
+
+  bool sparse_targets(uint64_t& mism) {
+    reset_ctl();
+    ws.push_ctl();
+    const uint32_t max_up = x_cap();
+    uint32_t* fa = list(2);
+    uint32_t* fb = list(3);
+    uint32_t* up = lab(2);
+    uint32_t* upidx = fin(0);
+    uint64_t* pv = reinterpret_cast<uint64_t*>(list(2));
+    // 1. crossing lists X for both families: re-evaluate only 64-vertex chunks
+    //    whose codes changed since the last X (cdirty, set by every writer)
+    const bool incremental = x_valid;
+    uint32_t nxs[2];
+    CK(cudaMemsetAsync(ws.ctl->sp_count, 0, 4 * sizeof(uint32_t), ws.stream));
+    if (incremental) {
+      pre(kProfSparse);
+      k_cross_chunks<<<grid_for(uint64_t(x_n[0]) + x_n[1] + n() / 64, 256, ws.sms, 16), 256, 0,
+                       ws.stream>>>(s.gdir, s.fM, s.fm, geo, s.cdirty, xlist(0, x_cur[0]), x_n[0],
+                                    xlist(1, x_cur[1]), x_n[1], xlist(0, x_cur[0] ^ 1),
+                                    xlist(1, x_cur[1] ^ 1), ws.ctl->sp_count, x_cap());
+      launched(kProfSparse);
+    } else {
+      for (int fam = 0; fam < 2; ++fam) {
+        const uint32_t* fL = fam ? s.fm : s.fM;
+        uint32_t* out = xlist(fam, x_cur[fam] ^ 1);
+        uint32_t* cnt = &ws.ctl->sp_count[fam];
+        pre(kProfSparse);
+        if (geo.ndims == 2)
+          k_cross<2><<<grid_for(n(), 256, ws.sms, 16), 256, 0, ws.stream>>>(s.gdir, fL, geo, fam,
+                                                                           out, cnt, x_cap());
+        else
+          k_cross<3><<<grid_for(n(), 256, ws.sms, 16), 256, 0, ws.stream>>>(s.gdir, fL, geo, fam,
+                                                                           out, cnt, x_cap());
+        launched(kProfSparse);
+      }
+    }
+    CK(cudaMemsetAsync(s.cdirty, 0, (n() + 2047) / 2048 * 4, ws.stream));
+    CK(cudaMemcpyAsync(nxs, ws.ctl->sp_count, sizeof nxs, cudaMemcpyDeviceToHost, ws.stream));
+    ws.sync();
+    x_valid = false;
+    for (int fam = 0; fam < 2; ++fam) {
+      if (trace) std::fprintf(stderr, "[mssz] sparse fam=%d |X|=%u%s\n", fam, nxs[fam],
+                              incremental ? " (incremental)" : "");
+      if (nxs[fam] > max_up) return false;
+    }
+    for (int fam = 0; fam < 2; ++fam) {
+      x_cur[fam] ^= 1;
+      x_n[fam] = nxs[fam];
+    }
+    x_valid = true;
+    // 2. per family: Up(X) by backward BFS, restricted labels, targets
+    for (int fam = 0; fam < 2; ++fam) {
+      const uint32_t mark = ws.next_mark++;
+      const uint32_t* fL = fam ? s.fm : s.fM;
+      const uint32_t nx = x_n[fam];
+      if (nx == 0) continue;  // no crossing step: every label of this family matches
+      CK(cudaMemsetAsync(ws.ctl->sp_count, 0, 4 * sizeof(uint32_t), ws.stream));
+      CK(cudaMemcpyAsync(fa, xlist(fam, x_cur[fam]), size_t(nx) * 4, cudaMemcpyDeviceToDevice,
+                         ws.stream));
+      CK(cudaMemcpyAsync(&ws.ctl->sp_count[1], &x_n[fam], 4, cudaMemcpyHostToDevice, ws.stream));
+      CK(cudaMemcpyAsync(&ws.ctl->sp_count[3], &nx, 4, cudaMemcpyHostToDevice, ws.stream));
+      pre(kProfSparse);
+      k_up_seed<<<grid_for(nx, 256, ws.sms, 16), 256, 0, ws.stream>>>(fa, nx, s.fmark, mark, up);
+      launched(kProfSparse);
+      // backward BFS (cooperative)
+      int occ = 0;
+      void* fn = geo.ndims == 2 ? (void*)k_upstream<2> : (void*)k_upstream<3>;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 512, 0));
+      const int blocks = ws.sms * std::max(1, std::min(occ, 2));
+      Geom gg = geo;
+      const uint8_t* gd = s.gdir;
+      uint32_t* fmk = s.fmark;
+      uint32_t mk = mark, mu = max_up, ml = kSparseMaxLevels;
+      Ctl* ctl = ws.ctl;
+      void* args[] = {(void*)&gd, &gg, &fam, &fmk, &mk, &fa, &fb, &up, &mu, &ml, &ctl};
+      pre(kProfSparse);
+      CK(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(512), args, 0, ws.stream));
+      launched(kProfSparse);
+      ws.pull_ctl();
+      if (trace)
+        std::fprintf(stderr, "[mssz] sparse fam=%d |Up|=%u levels=%u abort=%u\n", fam,
+                     ws.hctl->sp_count[3], ws.hctl->sp_levels, ws.hctl->sp_abort);
+      if (ws.hctl->sp_abort) return false;
+      const uint32_t nup = ws.hctl->sp_count[3];
+      st.sparse_up += nup;
+      pre(kProfSparse);
+      k_up_index<<<grid_for(nup, 256, ws.sms, 16), 256, 0, ws.stream>>>(up, nup, upidx);
+      launched(kProfSparse);
+      pre(kProfSparse);
+      k_up_parent<<<grid_for(nup, 256, ws.sms, 16), 256, 0, ws.stream>>>(up, nup, s.gdir, geo, fam,
+                                                                         s.fmark, mark, upidx, fL, pv);
+      launched(kProfSparse);
+      for (int round = 0;; round += 4) {
+        CK(cudaMemsetAsync(ws.ctl->flags, 0, 4 * sizeof(uint32_t), ws.stream));
+        for (int r = 0; r < 4; ++r) {
+          pre(kProfSparse);
+          k_up_jump<<<grid_for(nup, 256, ws.sms, 16), 256, 0, ws.stream>>>(pv, nup, &ws.ctl->flags[r]);
+          launched(kProfSparse);
+        }
+        uint32_t flags[4];
+        CK(cudaMemcpyAsync(flags, ws.ctl->flags, sizeof flags, cudaMemcpyDeviceToHost, ws.stream));
+        ws.sync();
+        if (!flags[3]) break;
+        if (round > 70) fail(MSSZ_CU_ERR_INTERNAL, "integral line cycle in the sparse R pass");
+      }
+      pre(kProfSparse);
+      k_up_targets<T><<<grid_for(nup, 256, ws.sms, 16), 256, 0, ws.stream>>>(s, up, nup, fam, pv,
+                                                                             list(0));
+      launched(kProfSparse);
+    }
+    ws.pull_ctl();
+    if (ws.hctl->status == kStatusTroubleMax)
+      fail(MSSZ_CU_ERR_INTERNAL, "troublemaker target is an extremum (stale critical report)");
+    mism = ws.hctl->mism;
+    ++st.sparse_iterations;
+    return true;
+  }
+
+  // run_r_loop (edit_engine.cpp:329-366).  Returns true when it stopped on
+  // matching labels (the outer loop's postcondition), false on new false CPs.
+  // Incremental after the first iteration: only label tiles whose direction
+  // codes changed are re-resolved, and only tiles that are dirty or whose exits
+  // changed their final label recompute their mismatch bits.
   bool run_r_loop() {
     uint64_t iters = 0;
+    bool first = true;
+    TileStore ts = tile_store();
+    struct DirtyOff {
+      State<T>& s;
+      ~DirtyOff() { s.tdirty = nullptr; }
+    } dirty_off{s};
+    s.tdirty = ts.dirty;
+    uint64_t& last_mism = r_last_mism;  // persists across run_r_loop calls
+    bool& full_valid = r_full_valid;     // incremental full-pass state is current
+    bool last_frontier = false;          // the previous batch refreshed via k_frontier
     for (;;) {
-      if (count_false_critical() != 0) return false;
-      labels_from_codes(s.gdir, lab(2), lab(3), false);
-      reset_ctl();
-      ws.push_ctl();
-      pre(kProfRfix);
-      k_rfix<T><<<grid_for(n() / 4 + 1, 256, ws.sms, 16), 256, 0, ws.stream>>>(s, list(0));
-      launched(kProfRfix);
-      ws.pull_ctl();
-      const Ctl c = *ws.hctl;
-      if (c.status == kStatusTroubleMax)
-        fail(MSSZ_CU_ERR_INTERNAL, "troublemaker target is an extremum (stale critical report)");
-      if (c.mism == 0) return true;
+      const auto t_it = std::chrono::steady_clock::now();
+      // the C-loop that precedes this call ended with every kind empty, so the
+      // gate (edit_engine.cpp:338) can only fire after one of our own batches
+      if (!first && count_false_critical(/*frontier_only=*/last_frontier) != 0) return false;
+      uint64_t mism = 0;
+      bool done = false;
+      const bool try_sparse = last_mism < n() / kSparseMismDivisor;
+      if (trace)
+        std::fprintf(stderr, "[mssz] R decide first=%d last_mism=%llu limit=%u sparse=%d\n", int(first),
+                     (unsigned long long)last_mism, n() / kSparseMismDivisor, int(try_sparse));
+      if (try_sparse) done = sparse_targets(mism);
+      if (!done) {
+        label_pass(s.gdir, lab(2), lab(3), /*only_dirty=*/full_valid, /*finish=*/false);
+        mism = r_targets(/*all_tiles=*/!full_valid);
+        full_valid = true;
+      } else {
+        full_valid = false;
+        CK(cudaMemsetAsync(ts.dirty, 0, ts.ntiles, ws.stream));
+      }
+      first = false;
+      last_mism = mism;
+      if (mism == 0) return true;
       if (++iters > opt.r_cap) fail(MSSZ_CU_ERR_NON_CONVERGENCE, "R-loop exceeded its iteration cap");
       // claim each distinct target once and lower it (edit_engine.cpp:344-358)
-      const uint32_t ntargets = c.list_count[0];
+      const uint32_t ntargets = ws.hctl->list_count[0];
       const uint32_t batch = ws.next_batch++;
+      CK(cudaMemsetAsync(&ws.ctl->s_count, 0, 2 * sizeof(uint32_t), ws.stream));
       pre(kProfFix);
       k_fix_list<T><<<grid_for(ntargets, 256, ws.sms, 16), 256, 0, ws.stream>>>(s, list(0), ntargets,
                                                                                 0, batch);
@@ -630,7 +929,10 @@ struct Engine {
       const uint32_t mark = ws.next_mark++;
       if (applied > n() / kHugeBatchDivisor) {
         directions(s.g, s.gdir);  // large batch: one streaming sweep beats 15 RMWs per edit
+        CK(cudaMemsetAsync(ts.dirty, 1, ts.ntiles, ws.stream));
+        last_frontier = false;
       } else {
+        last_frontier = true;
         pre(kProfFrontier);
         if (geo.ndims == 2)
           k_frontier<T, 2><<<grid_for(uint64_t(applied) * 8, 256, ws.sms, 16), 256, 0, ws.stream>>>(s, applied, mark);
@@ -640,6 +942,11 @@ struct Engine {
       }
       st.effective_edits += applied;
       ++st.r_iterations;
+      if (trace)
+        std::fprintf(stderr, "[mssz] R it=%llu mism=%llu targets=%u applied=%u tiles=%llu/%llu %.2f ms\n",
+                     (unsigned long long)st.r_iterations, (unsigned long long)mism, ntargets,
+                     applied, (unsigned long long)st.label_tiles, (unsigned long long)st.rfix_tiles,
+                     1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t_it).count());
       on_batch();
     }
   }
@@ -671,7 +978,7 @@ struct Engine {
     directions(d_f, ws.fdir.as<uint8_t>());
     directions(s.g, s.gdir);
     CK(cudaEventRecord(ws.ev[1], ws.stream));
-    labels_from_codes(s.fdir, lab(0), lab(1), true);
+    label_pass(s.fdir, lab(0), lab(1), false, true);
     {
       float ms = 0;
       CK(cudaEventElapsedTime(&ms, ws.ev[0], ws.ev[1]));
@@ -702,14 +1009,8 @@ struct Engine {
     if (!labels_verified) {
       if (count_false_critical() != 0)
         fail(MSSZ_CU_ERR_INTERNAL, "converged with false critical points");
-      labels_from_codes(s.gdir, lab(2), lab(3), false);
-      reset_ctl();
-      ws.push_ctl();
-      pre(kProfRfix);
-      k_rfix<T><<<grid_for(n() / 4 + 1, 256, ws.sms, 16), 256, 0, ws.stream>>>(s, list(0));
-      launched(kProfRfix);
-      ws.pull_ctl();
-      if (ws.hctl->mism != 0) fail(MSSZ_CU_ERR_INTERNAL, "converged with mismatched labels");
+      label_pass(s.gdir, lab(2), lab(3), false, false);
+      if (r_targets(true) != 0) fail(MSSZ_CU_ERR_INTERNAL, "converged with mismatched labels");
     }
   }
 

@@ -34,6 +34,9 @@ struct Ctl {
   uint32_t cmd_it;
   uint32_t pad_;
   uint64_t big_batches;  // batches that ran grid-wide
+  uint32_t sp_count[4];  // sparse R-loop: X / frontier (2) / Up sizes
+  uint32_t sp_abort;
+  uint32_t sp_levels;
 };
 
 enum : uint32_t {
@@ -43,6 +46,26 @@ enum : uint32_t {
   kStatusTroubleMax = 3,   // "troublemaker target is an extremum" (:305-306)
   kStatusHuge = 4,         // k_subloop handed a huge batch back to the host
 };
+
+// Label tiles (K3): 8192 vertices, power-of-two extents.
+template <int DIM>
+struct LabelTile;
+template <>
+struct LabelTile<2> {
+  static constexpr int TX = 128, TY = 64, TZ = 1, LX = 7, LY = 6;
+  static constexpr int kSurface = 2 * (TX + TY);
+};
+template <>
+struct LabelTile<3> {
+  static constexpr int TX = 32, TY = 16, TZ = 16, LX = 5, LY = 4;
+  static constexpr int kSurface = 2 * (TX * TY + TY * TZ + TX * TZ);
+};
+template <int DIM>
+__device__ __forceinline__ uint32_t label_tile_of(const Geom& g, uint32_t x, uint32_t y, uint32_t z) {
+  using TL = LabelTile<DIM>;
+  const uint32_t ntx = (g.X + TL::TX - 1) / TL::TX, nty = (g.Y + TL::TY - 1) / TL::TY;
+  return x / TL::TX + ntx * (y / TL::TY + nty * (DIM == 2 ? 0u : z / TL::TZ));
+}
 
 template <class T>
 struct State;
@@ -368,6 +391,8 @@ struct State {
   const uint32_t* gm;
   double xi;
   Ctl* ctl;
+  uint8_t* tdirty;  // R-loop only: label tiles whose direction codes changed
+  uint32_t* cdirty; // 1 bit per 64-vertex chunk whose codes changed (sparse R pass's X)
 };
 
 // claim (edit_engine.cpp:160-169) + lower_step (:75-86): the first claimant of
@@ -387,18 +412,45 @@ template <class T>
 __device__ __forceinline__ void fix_batch(const State<T>& s, const uint32_t* __restrict__ list,
                                           uint32_t n, int rule, uint32_t batch, uint32_t* s_count,
                                           uint64_t tid, uint64_t stride) {
-  for (uint64_t wb = tid & ~uint64_t(31); wb < n; wb += stride) {
-    const uint64_t i = wb + (threadIdx.x & 31);
-    bool ok = false;
-    uint32_t t = 0;
-    if (i < n) {
-      const uint32_t v = __ldcg(list + i);
-      if (rule == 0) t = v;
-      else if (rule == 1) t = v + s.geo.off[__ldcg(s.gdir + v) & 15u];
-      else t = v + s.geo.off[__ldg(s.fdir + v) >> 4];
-      ok = claim_and_lower(s, t, batch);
+  // two list items per lane per step: their loads and claims overlap
+  const uint64_t step = 2 * stride;
+  for (uint64_t wb = (tid & ~uint64_t(31)) * 2; wb < n; wb += step) {
+    const uint64_t i0 = wb + (threadIdx.x & 31), i1 = i0 + 32;
+    uint32_t t[2] = {0, 0};
+    bool live[2] = {i0 < n, i1 < n};
+    uint32_t v[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) v[j] = live[j] ? __ldcg(list + (j ? i1 : i0)) : 0u;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      if (!live[j]) continue;
+      if (rule == 0) t[j] = v[j];
+      else if (rule == 1) t[j] = v[j] + s.geo.off[__ldcg(s.gdir + v[j]) & 15u];
+      else t[j] = v[j] + s.geo.off[__ldg(s.fdir + v[j]) >> 4];
     }
-    warp_append(ok, t, s.S, s_count);
+    uint32_t prev[2] = {batch, batch};
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      if (live[j]) prev[j] = atomicExch(&s.stamp[t[j]], batch);
+    T gv[2], fv[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      if (prev[j] != batch) {
+        gv[j] = __ldcg(s.g + t[j]);
+        fv[j] = __ldg(s.f + t[j]);
+      }
+    bool ok[2] = {false, false};
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      T nv;
+      if (prev[j] != batch && lower_value<T>(gv[j], fv[j], s.xi, nv)) {
+        s.g[t[j]] = nv;
+        s.touched[t[j]] = 1;
+        ok[j] = true;
+      }
+    }
+    warp_append(ok[0], t[0], s.S, s_count);
+    warp_append(ok[1], t[1], s.S, s_count);
   }
 }
 
@@ -446,8 +498,16 @@ __device__ __forceinline__ void frontier_update(const State<T>& s, uint32_t ns, 
           u = ux + s.geo.X * uy + s.geo.XY * uz;
           if (__ldcg(s.fmark + u) != mark && atomicExch(&s.fmark[u], mark) != mark) {
             mine = true;
-            s.gdir[u] =
+            const uint8_t code =
                 static_cast<uint8_t>(direction_code<T, DIM, true>(s.g, s.geo, u, ux, uy, uz));
+            if (s.gdir[u] != code) {
+              s.gdir[u] = code;
+              if (s.tdirty) s.tdirty[label_tile_of<DIM>(s.geo, ux, uy, uz)] = 1;
+              if (s.cdirty) {  // test first: neighbouring edits share the chunk bit
+                const uint32_t bit = 1u << ((u >> 6) & 31);
+                if (!(s.cdirty[u >> 11] & bit)) atomicOr(&s.cdirty[u >> 11], bit);
+              }
+            }
           }
         }
       }
@@ -768,18 +828,6 @@ __global__ void __launch_bounds__(256) k_label_jump(uint32_t* __restrict__ M,
 //  3. k_label_finish: one gather per vertex, lab[v] = lab[lab[v]].
 // The fixpoint is the chain terminus, identical to the reference's
 // round-synchronous doubling (mss.cpp:60-80).
-template <int DIM>
-struct LabelTile;
-template <>
-struct LabelTile<2> {
-  static constexpr int TX = 128, TY = 64, TZ = 1, LX = 7, LY = 6;
-  static constexpr int kSurface = 2 * (TX + TY);
-};
-template <>
-struct LabelTile<3> {
-  static constexpr int TX = 32, TY = 16, TZ = 16, LX = 5, LY = 4;
-  static constexpr int kSurface = 2 * (TX * TY + TY * TZ + TX * TZ);
-};
 constexpr int kLabelTileN = 8192;
 constexpr int kLabelTileThreads = 512;
 template <int DIM>
@@ -787,11 +835,27 @@ constexpr size_t label_tile_smem() {
   return kLabelTileN * 4 + 2 * LabelTile<DIM>::kSurface * 4 + kLabelTileN;
 }
 
+// Per-tile label state kept across R-loop iterations (incremental labels).
+struct TileStore {
+  uint32_t* E;        // [ntiles][2][kSurface] distinct exits of the tile per family
+  uint32_t* Ecnt;     // [ntiles][2]
+  uint32_t* oldfin;   // [ntiles][2][kSurface] exit finals of the previous pass
+  uint8_t* dirty;     // [ntiles] a direction code in the tile changed
+  uint8_t* affected;  // [ntiles] an exit of the tile changed its final label
+  uint32_t* mis_bits; // [ntiles][2][kLabelTileN / 32] divergent-and-mismatched bits
+  uint32_t* mis_cnt;  // [ntiles]
+  uint32_t ntiles;
+  uint32_t surface;   // LabelTile<DIM>::kSurface
+};
+
+// Phase 1.  Writes the provisional label (root, or first vertex outside the
+// tile) to prov and fin, and the tile's distinct exits to the tile store.
+// tile_list == nullptr: CTA i handles tile i.
 template <int DIM>
 __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
     const uint8_t* __restrict__ dir, Geom g, uint32_t* __restrict__ M, uint32_t* __restrict__ m,
-    uint32_t* __restrict__ mark, uint32_t mark_asc, uint32_t* __restrict__ E_asc,
-    uint32_t* __restrict__ E_desc, uint32_t* counts /* [0] asc, [1] desc */) {
+    uint32_t* __restrict__ finM, uint32_t* __restrict__ finm, const uint32_t* tile_list,
+    TileStore ts) {
   using TL = LabelTile<DIM>;
   constexpr int NS = StencilSize<DIM>::value;
   constexpr int PER = kLabelTileN / kLabelTileThreads;
@@ -804,7 +868,12 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
   uint32_t (*sexit)[LabelTile<DIM>::kSurface] =
       reinterpret_cast<uint32_t (*)[LabelTile<DIM>::kSurface]>(ptr + kLabelTileN);
   uint8_t* sdir = reinterpret_cast<uint8_t*>(ptr + kLabelTileN + 2 * LabelTile<DIM>::kSurface);
-  __shared__ uint32_t sexit_n[2], sexit_base[2];
+  __shared__ uint32_t sexit_n[2];
+  // per-family bitmap over the tile's halo box: each distinct exit is listed once per tile
+  constexpr int HBOX = (TL::TX + 2) * (TL::TY + 2) * (DIM == 2 ? 1 : TL::TZ + 2);
+  __shared__ uint32_t seen[2][(HBOX + 31) / 32];
+  for (int w = threadIdx.x; w < 2 * ((HBOX + 31) / 32); w += kLabelTileThreads)
+    (&seen[0][0])[w] = 0u;
   if (threadIdx.x < 2) sexit_n[threadIdx.x] = 0;
   __shared__ int8_t sd[3][16];
   __shared__ int32_t soff[16];
@@ -820,7 +889,7 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
   }
   const uint32_t ntx = (g.X + TL::TX - 1) / TL::TX;
   const uint32_t nty = (g.Y + TL::TY - 1) / TL::TY;
-  const uint32_t b = blockIdx.x;
+  const uint32_t b = tile_list ? tile_list[blockIdx.x] : blockIdx.x;
   const uint32_t tx = b % ntx, ty = (b / ntx) % nty, tz = b / (ntx * nty);
   const uint32_t x0 = tx * TL::TX, y0 = ty * TL::TY, z0 = tz * TL::TZ;
   const int ex = min(TL::TX, static_cast<int>(g.X - x0));
@@ -900,22 +969,119 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
                   tlz = t >> (TL::LX + TL::LY);
         const uint32_t res = base + tlx + g.X * tly + g.XY * tlz + soff[c];  // soff[15] = 0
         (fam ? m : M)[gi] = res;
-        if (t == i && c != kSelf) sexit[fam][atomicAdd(&sexit_n[fam], 1u)] = res;
+        (fam ? finm : finM)[gi] = res;
+        if (t == i && c != kSelf) {
+          const int hx = tlx + sd[0][c] + 1, hy = tly + sd[1][c] + 1;
+          const int hz = DIM == 2 ? 0 : tlz + sd[2][c] + 1;
+          const int h = hx + (TL::TX + 2) * (hy + (TL::TY + 2) * hz);
+          if (!(atomicOr(&seen[fam][h >> 5], 1u << (h & 31)) & (1u << (h & 31))))
+            sexit[fam][atomicAdd(&sexit_n[fam], 1u)] = res;
+        }
       }
     }
   }
   __syncthreads();
-  if (threadIdx.x < 2 && sexit_n[threadIdx.x])
-    sexit_base[threadIdx.x] = atomicAdd(counts + threadIdx.x, sexit_n[threadIdx.x]);
-  __syncthreads();
 #pragma unroll
   for (int fam = 0; fam < 2; ++fam) {
-    uint32_t* E = fam ? E_desc : E_asc;
-    for (uint32_t k = threadIdx.x; k < sexit_n[fam]; k += kLabelTileThreads)
-      E[sexit_base[fam] + k] = sexit[fam][k];
+    uint32_t* E = ts.E + (static_cast<size_t>(b) * 2 + fam) * LabelTile<DIM>::kSurface;
+    for (uint32_t k = threadIdx.x; k < sexit_n[fam]; k += kLabelTileThreads) E[k] = sexit[fam][k];
+    if (threadIdx.x == 0) ts.Ecnt[b * 2 + fam] = sexit_n[fam];
   }
-  (void)mark;
-  (void)mark_asc;
+}
+
+// Phase 2a (all tiles): remember every exit's final label (k_exit_save), then
+// restart it from the provisional one (k_exit_reset).  Two launches, so an exit
+// listed by several tiles is saved before any tile resets it.  CTA per tile.
+__global__ void __launch_bounds__(256) k_exit_save(TileStore ts, const uint32_t* __restrict__ finM,
+                                                   const uint32_t* __restrict__ finm) {
+  const uint32_t b = blockIdx.x;
+#pragma unroll
+  for (int fam = 0; fam < 2; ++fam) {
+    const uint32_t n = ts.Ecnt[b * 2 + fam];
+    const size_t o = (static_cast<size_t>(b) * 2 + fam) * ts.surface;
+    const uint32_t* fin = fam ? finm : finM;
+    for (uint32_t k = threadIdx.x; k < n; k += blockDim.x) ts.oldfin[o + k] = fin[ts.E[o + k]];
+  }
+}
+
+__global__ void __launch_bounds__(256) k_exit_reset(TileStore ts, const uint32_t* __restrict__ M,
+                                                    const uint32_t* __restrict__ m,
+                                                    uint32_t* __restrict__ finM,
+                                                    uint32_t* __restrict__ finm) {
+  const uint32_t b = blockIdx.x;
+#pragma unroll
+  for (int fam = 0; fam < 2; ++fam) {
+    const uint32_t n = ts.Ecnt[b * 2 + fam];
+    const size_t o = (static_cast<size_t>(b) * 2 + fam) * ts.surface;
+    uint32_t* fin = fam ? finm : finM;
+    const uint32_t* prov = fam ? m : M;
+    for (uint32_t k = threadIdx.x; k < n; k += blockDim.x) {
+      const uint32_t e = ts.E[o + k];
+      fin[e] = prov[e];
+    }
+  }
+}
+
+// Phase 2b: first doubling round straight from the tile stores; unresolved
+// exits go to the compact lists that k_label_exit_jump keeps halving.
+__global__ void __launch_bounds__(256) k_exit_jump_tiles(TileStore ts, uint32_t* __restrict__ finM,
+                                                         uint32_t* __restrict__ finm,
+                                                         uint32_t* __restrict__ out_a,
+                                                         uint32_t* __restrict__ out_d,
+                                                         uint32_t* cnt_out) {
+  const uint32_t b = blockIdx.x;
+  for (int fam = 0; fam < 2; ++fam) {
+    const uint32_t n = ts.Ecnt[b * 2 + fam];
+    const size_t o = (static_cast<size_t>(b) * 2 + fam) * ts.surface;
+    uint32_t* fin = fam ? finm : finM;
+    for (uint32_t kb = threadIdx.x & ~31u; kb < n; kb += blockDim.x) {
+      const uint32_t k = kb + (threadIdx.x & 31);
+      bool keep = false;
+      uint32_t e = 0;
+      if (k < n) {
+        e = ts.E[o + k];
+        const uint32_t l = fin[e];
+        const uint32_t ll = fin[l];
+        if (ll != l) {
+          fin[e] = ll;
+          keep = fin[ll] != ll;
+        }
+      }
+      warp_append(keep, e, fam ? out_d : out_a, cnt_out + fam);
+    }
+  }
+}
+
+// Phase 2c: tiles whose exits changed their final label are "affected".
+__global__ void __launch_bounds__(256) k_exit_changed(TileStore ts, const uint32_t* __restrict__ finM,
+                                                      const uint32_t* __restrict__ finm) {
+  const uint32_t b = blockIdx.x;
+  bool changed = false;
+  for (int fam = 0; fam < 2; ++fam) {
+    const uint32_t n = ts.Ecnt[b * 2 + fam];
+    const size_t o = (static_cast<size_t>(b) * 2 + fam) * ts.surface;
+    const uint32_t* fin = fam ? finm : finM;
+    for (uint32_t k = threadIdx.x; k < n; k += blockDim.x)
+      changed |= fin[ts.E[o + k]] != ts.oldfin[o + k];
+  }
+  if (__syncthreads_or(changed) && threadIdx.x == 0) ts.affected[b] = 1;
+}
+
+// Tile selection: mode 0 dirty, 1 dirty|affected, 2 mis_cnt > 0.
+__global__ void __launch_bounds__(256) k_select_tiles(TileStore ts, int mode, uint32_t* out,
+                                                      uint32_t* count) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t wb = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) & ~uint64_t(31);
+       wb < ts.ntiles; wb += stride) {
+    const uint64_t t = wb + (threadIdx.x & 31);
+    bool sel = false;
+    if (t < ts.ntiles) {
+      if (mode == 0) sel = ts.dirty[t];
+      else if (mode == 1) sel = ts.dirty[t] || ts.affected[t];
+      else sel = ts.mis_cnt[t] != 0;
+    }
+    warp_append(sel, static_cast<uint32_t>(t), out, count);
+  }
 }
 
 // One doubling round over the unresolved exits: in[] -> out[] keeps only
@@ -955,25 +1121,24 @@ __global__ void __launch_bounds__(256) k_label_exit_jump(uint32_t* __restrict__ 
   }
 }
 
+// Phase 3 (f labels only): final label of every vertex, lab[v] = fin[lab[v]].
 __global__ void __launch_bounds__(256) k_label_finish(uint32_t* __restrict__ M,
-                                                      uint32_t* __restrict__ m, uint32_t n) {
+                                                      uint32_t* __restrict__ m,
+                                                      const uint32_t* __restrict__ finM,
+                                                      const uint32_t* __restrict__ finm, uint32_t n) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   const uint64_t n4 = n / 4;
   for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n4;
        q += stride) {
-    uint4 a = reinterpret_cast<const uint4*>(M)[q];
-    uint4 d = reinterpret_cast<const uint4*>(m)[q];
-    const uint32_t a2[4] = {M[a.x], M[a.y], M[a.z], M[a.w]};
-    const uint32_t d2[4] = {m[d.x], m[d.y], m[d.z], m[d.w]};
-    if (a2[0] != a.x || a2[1] != a.y || a2[2] != a.z || a2[3] != a.w)
-      reinterpret_cast<uint4*>(M)[q] = make_uint4(a2[0], a2[1], a2[2], a2[3]);
-    if (d2[0] != d.x || d2[1] != d.y || d2[2] != d.z || d2[3] != d.w)
-      reinterpret_cast<uint4*>(m)[q] = make_uint4(d2[0], d2[1], d2[2], d2[3]);
+    const uint4 a = reinterpret_cast<const uint4*>(M)[q];
+    const uint4 d = reinterpret_cast<const uint4*>(m)[q];
+    reinterpret_cast<uint4*>(M)[q] = make_uint4(finM[a.x], finM[a.y], finM[a.z], finM[a.w]);
+    reinterpret_cast<uint4*>(m)[q] = make_uint4(finm[d.x], finm[d.y], finm[d.z], finm[d.w]);
   }
   for (uint64_t v = n4 * 4 + static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < n;
        v += stride) {
-    M[v] = M[M[v]];
-    m[v] = m[m[v]];
+    M[v] = finM[M[v]];
+    m[v] = finm[m[v]];
   }
 }
 
@@ -1017,78 +1182,329 @@ __global__ void k_u32_to_u64(const uint32_t* __restrict__ in, uint64_t* __restri
 // ctl->mism counts divergent mismatched vertices: it is zero exactly when no
 // vertex is mismatched (the walk argument above), which is the reference's
 // collect_mismatched() == 0 test.
-template <class T>
-__global__ void __launch_bounds__(256) k_rfix(State<T> s, uint32_t* __restrict__ targets) {
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+// Tile pass: for every vertex of the listed tiles, is it divergent AND
+// mismatched (per family)?  One warp = 32 consecutive tile-local vertices =
+// one bitmap word (ballot).  Final g labels are fin[prov[v]] (prov = gM/gm).
+// Tiles not listed keep last iteration's bitmap: neither their directions
+// (not dirty) nor the finals of the exits their chains leave through (not
+// affected) changed, so their mismatch set is unchanged.
+template <class T, int DIM>
+__global__ void __launch_bounds__(256) k_rfix_tiles(State<T> s, const uint32_t* __restrict__ tiles,
+                                                    TileStore ts, const uint32_t* __restrict__ finM,
+                                                    const uint32_t* __restrict__ finm) {
+  using TL = LabelTile<DIM>;
+  const Geom& g = s.geo;
+  const uint32_t ntx = (g.X + TL::TX - 1) / TL::TX;
+  const uint32_t nty = (g.Y + TL::TY - 1) / TL::TY;
+  const uint32_t b = tiles ? tiles[blockIdx.x] : blockIdx.x;
+  const uint32_t tx = b % ntx, ty = (b / ntx) % nty, tz = b / (ntx * nty);
+  const uint32_t x0 = tx * TL::TX, y0 = ty * TL::TY, z0 = tz * TL::TZ;
+  const int ex = min(TL::TX, static_cast<int>(g.X - x0));
+  const int ey = min(TL::TY, static_cast<int>(g.Y - y0));
+  const int ez = DIM == 2 ? 1 : min(TL::TZ, static_cast<int>(g.Z - z0));
+  const uint32_t base = x0 + g.X * y0 + g.XY * z0;
+  uint32_t* bits = ts.mis_bits + static_cast<size_t>(b) * 2 * (kLabelTileN / 32);
+  uint32_t cnt = 0;
+  for (int i = threadIdx.x; i < kLabelTileN; i += blockDim.x) {
+    const int lx = i & (TL::TX - 1), ly = (i >> TL::LX) & (TL::TY - 1), lz = i >> (TL::LX + TL::LY);
+    bool ma = false, md = false;
+    if (lx < ex && ly < ey && lz < ez) {
+      const uint32_t v = base + lx + g.X * ly + g.XY * lz;
+      const uint32_t fc = __ldg(s.fdir + v), gc = __ldg(s.gdir + v);
+      const bool wa = (gc & 15u) != (fc & 15u);  // ascending line diverges at v
+      const bool wd = (gc >> 4) != (fc >> 4);    // descending line diverges at v
+      uint32_t la = 0, ld = 0, fa = 0, fd = 0;
+      if (wa) {
+        la = __ldg(s.gM + v);
+        fa = __ldg(s.fM + v);
+      }
+      if (wd) {
+        ld = __ldg(s.gm + v);
+        fd = __ldg(s.fm + v);
+      }
+      ma = wa && __ldg(finM + la) != fa;
+      md = wd && __ldg(finm + ld) != fd;
+    }
+    const uint32_t wa_bits = __ballot_sync(0xffffffffu, ma);
+    const uint32_t wd_bits = __ballot_sync(0xffffffffu, md);
+    if ((threadIdx.x & 31) == 0) {
+      bits[i >> 5] = wa_bits;
+      bits[kLabelTileN / 32 + (i >> 5)] = wd_bits;
+      cnt += __popc(wa_bits) + __popc(wd_bits);
+    }
+  }
+  __shared__ uint32_t scnt;
+  if (threadIdx.x == 0) scnt = 0;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&scnt, cnt);
+  __syncthreads();
+  if (threadIdx.x == 0) ts.mis_cnt[b] = scnt;
+}
+
+// Targets of the R batch from the mismatch bitmaps of the listed tiles
+// (find_troublemaker's (v_i, v_t) for every falsely labelled vertex, see the
+// argument above): ascending -> g's ascending neighbour, descending -> f's
+// descending neighbour.  Also returns the total mismatch count in ctl->mism.
+template <class T, int DIM>
+__global__ void __launch_bounds__(256) k_expand_targets(State<T> s, const uint32_t* __restrict__ tiles,
+                                                        TileStore ts, uint32_t* __restrict__ targets,
+                                                        uint32_t* count) {
+  using TL = LabelTile<DIM>;
+  const Geom& g = s.geo;
+  const uint32_t ntx = (g.X + TL::TX - 1) / TL::TX;
+  const uint32_t nty = (g.Y + TL::TY - 1) / TL::TY;
+  const uint32_t b = tiles[blockIdx.x];
+  const uint32_t tx = b % ntx, ty = (b / ntx) % nty, tz = b / (ntx * nty);
+  const uint32_t base = tx * TL::TX + g.X * (ty * TL::TY) + g.XY * (tz * TL::TZ);
+  const uint32_t* bits = ts.mis_bits + static_cast<size_t>(b) * 2 * (kLabelTileN / 32);
   uint32_t mism = 0;
-  const uint32_t n = s.geo.n;
-  const uint64_t nq = (static_cast<uint64_t>(n) + 3) / 4;
-  for (uint64_t wb = tid & ~uint64_t(31); wb < nq; wb += stride) {
-    const uint64_t q = wb + (threadIdx.x & 31);
-    uint32_t fw = 0xFFFFFFFFu, gw = 0xFFFFFFFFu;
-    if (q < nq) {
-      if (q * 4 + 4 <= n) {
-        fw = __ldg(reinterpret_cast<const uint32_t*>(s.fdir) + q);
-        gw = __ldg(reinterpret_cast<const uint32_t*>(s.gdir) + q);
-      } else {
-        fw = gw = 0;
-        for (int j = 0; j < 4; ++j) {
-          const uint32_t fb = q * 4 + j < n ? s.fdir[q * 4 + j] : 0xFFu;
-          const uint32_t gb = q * 4 + j < n ? s.gdir[q * 4 + j] : 0xFFu;
-          fw |= fb << (8 * j);
-          gw |= gb << (8 * j);
+  for (int w = threadIdx.x; w < 2 * (kLabelTileN / 32); w += blockDim.x) {  // warp-uniform trip count
+    uint32_t word = bits[w];
+    const int fam = w >= kLabelTileN / 32;
+    mism += __popc(word);
+    const uint32_t pos0 = warp_reserve(__popc(word), count);
+    uint32_t pos = pos0;
+    while (word) {
+      const int j = __ffs(word) - 1;
+      word &= word - 1;
+      const int i = ((w % (kLabelTileN / 32)) << 5) + j;
+      const int lx = i & (TL::TX - 1), ly = (i >> TL::LX) & (TL::TY - 1), lz = i >> (TL::LX + TL::LY);
+      const uint32_t v = base + lx + g.X * ly + g.XY * lz;
+      const uint32_t code = fam ? (__ldg(s.fdir + v) >> 4) : (__ldg(s.gdir + v) & 15u);
+      if (code == kSelf) atomicExch(&s.ctl->status, kStatusTroubleMax);
+      targets[pos++] = code == kSelf ? v : v + g.off[code];
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mism += __shfl_xor_sync(0xffffffffu, mism, o);
+  if ((threadIdx.x & 31) == 0 && mism)
+    atomicAdd(reinterpret_cast<unsigned long long*>(&s.ctl->mism),
+              static_cast<unsigned long long>(mism));
+}
+
+// ---------------------------------------------------------------------------
+// Sparse R iteration (late R-loop iterations, few mismatches).
+//   X = { u : fL(step_g(u)) != fL(u) }: vertices whose g-step crosses an f-basin
+//   boundary (L = M with ascending steps, m with descending).  If a vertex's
+//   g-chain avoids X, fL is constant along it, so its g label equals its f
+//   label: every mismatched vertex lies in Up(X), the g-forest upstream
+//   closure of X.  At convergence X is empty.  So: list X, BFS backwards to
+//   Up(X), resolve g labels by pointer jumping restricted to Up(X) (a chain
+//   leaving Up(X) ends with the f label of its first outside vertex), and
+//   emit the batch targets of divergent mismatched vertices -- the same target
+//   set as the full pass.
+template <int DIM>
+__global__ void __launch_bounds__(256) k_cross(const uint8_t* __restrict__ gdir,
+                                               const uint32_t* __restrict__ fL, Geom g, int fam,
+                                               uint32_t* __restrict__ X, uint32_t* count,
+                                               uint32_t cap) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t wb = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) & ~uint64_t(31);
+       wb < g.n; wb += stride) {
+    const uint64_t v = wb + (threadIdx.x & 31);
+    bool cross = false;
+    if (v < g.n) {
+      const uint32_t c = (__ldg(gdir + v) >> (4 * fam)) & 15u;
+      if (c != kSelf) cross = __ldg(fL + v + g.off[c]) != __ldg(fL + v);
+    }
+    warp_append_cap(cross, static_cast<uint32_t>(v), X, count, cap);
+  }
+}
+
+// X maintained across any edits: both families at once.  Entries of the old
+// lists outside dirty chunks are kept; every vertex of a dirty chunk is
+// re-evaluated.  One warp per bitmap word; lanes cover a chunk's 64 vertices.
+__global__ void __launch_bounds__(256) k_cross_chunks(
+    const uint8_t* __restrict__ gdir, const uint32_t* __restrict__ fM,
+    const uint32_t* __restrict__ fm, Geom g, const uint32_t* __restrict__ cdirty,
+    const uint32_t* __restrict__ Xa_old, uint32_t na_old, const uint32_t* __restrict__ Xd_old,
+    uint32_t nd_old, uint32_t* __restrict__ Xa, uint32_t* __restrict__ Xd, uint32_t* counts,
+    uint32_t cap) {
+  const uint64_t gtid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  // (a) surviving old entries
+  const uint64_t nold = static_cast<uint64_t>(na_old) + nd_old;
+  for (uint64_t wb = gtid & ~uint64_t(31); wb < nold; wb += stride) {
+    const uint64_t i = wb + lane;
+    bool ka = false, kd = false;
+    uint32_t v = 0;
+    if (i < nold) {
+      v = i < na_old ? Xa_old[i] : Xd_old[i - na_old];
+      const bool clean = !((__ldg(cdirty + (v >> 11)) >> ((v >> 6) & 31)) & 1u);
+      ka = clean && i < na_old;
+      kd = clean && i >= na_old;
+    }
+    warp_append_cap(ka, v, Xa, counts + 0, cap);
+    warp_append_cap(kd, v, Xd, counts + 1, cap);
+  }
+  // (b) re-evaluate dirty chunks
+  const uint64_t nwords = (static_cast<uint64_t>(g.n) + 2047) / 2048;
+  const uint64_t wstride = stride / 32;
+  for (uint64_t w = gtid / 32; w < nwords; w += wstride) {
+    uint32_t bits = __ldg(cdirty + w);
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint64_t v = (w * 32 + b) * 64 + h * 32 + lane;
+        bool ca = false, cd = false;
+        if (v < g.n) {
+          const uint32_t code = __ldg(gdir + v);
+          const uint32_t a = code & 15u, d = code >> 4;
+          if (a != kSelf) ca = __ldg(fM + v + g.off[a]) != __ldg(fM + v);
+          if (d != kSelf) cd = __ldg(fm + v + g.off[d]) != __ldg(fm + v);
         }
+        warp_append_cap(ca, static_cast<uint32_t>(v), Xa, counts + 0, cap);
+        warp_append_cap(cd, static_cast<uint32_t>(v), Xd, counts + 1, cap);
       }
     }
-    // gather every label first (independent loads in flight), then claim
-    uint32_t ta[4], td[4];
-    bool wa[4], wd[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint32_t v = static_cast<uint32_t>(q * 4 + j);
-      const uint32_t fc = (fw >> (8 * j)) & 0xFFu, gc = (gw >> (8 * j)) & 0xFFu;
-      wa[j] = (gc & 15u) != (fc & 15u);  // ascending line diverges at v
-      wd[j] = (gc >> 4) != (fc >> 4);    // descending line diverges at v
-      ta[j] = wa[j] ? __ldg(s.gM + v) : 0u;
-      td[j] = wd[j] ? __ldg(s.gm + v) : 0u;
+  }
+}
+
+// Backward BFS over the g-forest of family fam from the frontier list in[]:
+// u joins when its g-step points at a frontier vertex.  Persistent
+// cooperative kernel, one grid barrier pair per level; every reached vertex is
+// also appended to up[].  Aborts (ctl->sp_abort) when |Up| exceeds max_up.
+template <int DIM>
+__global__ void __launch_bounds__(512, 2)
+    k_upstream(const uint8_t* __restrict__ gdir, Geom g, int fam, uint32_t* __restrict__ fmark,
+               uint32_t mark, uint32_t* __restrict__ fa, uint32_t* __restrict__ fb,
+               uint32_t* __restrict__ up, uint32_t max_up, uint32_t max_levels, Ctl* ctl) {
+  cg::grid_group grid = cg::this_grid();
+  constexpr int LPS = 16;
+  constexpr int NS = StencilSize<DIM>::value;
+  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  uint32_t* cnt = ctl->sp_count;  // [1], [2]: frontier sizes; [3]: |Up|
+  int cur = 0;
+  uint32_t levels = 0;
+  for (;;) {
+    const uint32_t n = *reinterpret_cast<volatile uint32_t*>(&cnt[1 + cur]);
+    if (n == 0) break;
+    if (*reinterpret_cast<volatile uint32_t*>(&cnt[3]) > max_up || levels >= max_levels) {
+      if (tid == 0) ctl->sp_abort = 1;
+      break;
     }
-    uint32_t fa[4], fd[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint32_t v = static_cast<uint32_t>(q * 4 + j);
-      fa[j] = wa[j] ? __ldg(s.fM + v) : 0u;
-      fd[j] = wd[j] ? __ldg(s.fm + v) : 0u;
-      ta[j] = wa[j] ? __ldg(s.gM + ta[j]) : 0u;
-      td[j] = wd[j] ? __ldg(s.gm + td[j]) : 0u;
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint32_t v = static_cast<uint32_t>(q * 4 + j);
-      const uint32_t fc = (fw >> (8 * j)) & 0xFFu, gc = (gw >> (8 * j)) & 0xFFu;
-      const bool ma = wa[j] && ta[j] != fa[j];
-      const bool md = wd[j] && td[j] != fd[j];
-      mism += (ma ? 1u : 0u) + (md ? 1u : 0u);
-      bool oka = false, okd = false;
-      uint32_t xa = 0, xd = 0;
-      if (ma) {
-        if ((gc & 15u) == kSelf) atomicExch(&s.ctl->status, kStatusTroubleMax);
-        else {
-          xa = v + s.geo.off[gc & 15u];
-          oka = true;
+    const uint32_t* in = cur ? fb : fa;
+    uint32_t* out = cur ? fa : fb;
+    const uint64_t total = static_cast<uint64_t>(n) * LPS;
+    for (uint64_t wb = tid & ~uint64_t(31); wb < total; wb += stride) {
+      const uint64_t i = wb + (threadIdx.x & 31);
+      bool mine = false;
+      uint32_t u = 0;
+      if (i < total) {
+        const int k = static_cast<int>(i % LPS);
+        if (k < NS) {
+          const uint32_t y = in[i / LPS];
+          uint32_t x, yy, z;
+          coords(g, y, x, yy, z);
+          int dx, dy, dz;
+          slot_delta<DIM>(k, dx, dy, dz);
+          const uint32_t ux = x + dx, uy = yy + dy, uz = z + dz;
+          if (ux < g.X && uy < g.Y && (DIM == 2 || uz < g.Z)) {
+            u = ux + g.X * uy + g.XY * uz;
+            const uint32_t c = (__ldg(gdir + u) >> (4 * fam)) & 15u;
+            // u's step is the opposite slot of k (slots come in +d/-d pairs)
+            if (c == static_cast<uint32_t>(k ^ 1) && __ldcg(fmark + u) != mark &&
+                atomicExch(fmark + u, mark) != mark)
+              mine = true;
+          }
         }
       }
-      if (md) {
-        if ((fc >> 4) == kSelf) atomicExch(&s.ctl->status, kStatusTroubleMax);
-        else {
-          xd = v + s.geo.off[fc >> 4];
-          okd = true;
-        }
-      }
-      // targets only; claims + lowering run afterwards in k_fix_list (rule self)
-      warp_append(oka, xa, targets, &s.ctl->list_count[0]);
-      warp_append(okd, xd, targets, &s.ctl->list_count[0]);
+      warp_append_cap(mine, u, out, &cnt[2 - cur], max_up);
+      warp_append_cap(mine, u, up, &cnt[3], max_up);
     }
+    grid.sync();
+    if (tid == 0) cnt[1 + cur] = 0;
+    cur ^= 1;
+    ++levels;
+    grid.sync();
+  }
+  if (tid == 0) ctl->sp_levels += levels;
+}
+
+__global__ void __launch_bounds__(256) k_up_seed(const uint32_t* __restrict__ X, uint32_t nx,
+                                                 uint32_t* __restrict__ fmark, uint32_t mark,
+                                                 uint32_t* __restrict__ up) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nx; i += stride) {
+    fmark[X[i]] = mark;
+    up[i] = X[i];
+  }
+}
+
+// Restricted labels over Up, packed pv[i] = parent << 32 | value: parent is the
+// Up index of i's g-step target when that target is in Up (fmark == mark);
+// otherwise parent = ~0 and value = fL of the target (its chain avoids X).
+// One 64-bit word per entry keeps in-place jumping race-free.
+__global__ void __launch_bounds__(256) k_up_index(const uint32_t* __restrict__ up, uint32_t nup,
+                                                  uint32_t* __restrict__ upidx) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nup; i += stride)
+    upidx[up[i]] = static_cast<uint32_t>(i);
+}
+
+constexpr uint64_t kUpNone = 0xFFFFFFFF00000000ull;
+
+__global__ void __launch_bounds__(256) k_up_parent(const uint32_t* __restrict__ up, uint32_t nup,
+                                                   const uint8_t* __restrict__ gdir, Geom g, int fam,
+                                                   const uint32_t* __restrict__ fmark, uint32_t mark,
+                                                   const uint32_t* __restrict__ upidx,
+                                                   const uint32_t* __restrict__ fL,
+                                                   uint64_t* __restrict__ pv) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nup; i += stride) {
+    const uint32_t v = up[i];
+    const uint32_t c = (__ldg(gdir + v) >> (4 * fam)) & 15u;
+    const uint32_t p = v + g.off[c];  // c != SELF: every Up vertex steps towards X
+    pv[i] = __ldg(fmark + p) == mark ? (static_cast<uint64_t>(upidx[p]) << 32)
+                                     : (kUpNone | __ldg(fL + p));
+  }
+}
+
+__global__ void __launch_bounds__(256) k_up_jump(uint64_t* __restrict__ pv, uint32_t nup,
+                                                 uint32_t* flag) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  bool changed = false;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nup; i += stride) {
+    const uint64_t w = pv[i];
+    if ((w >> 32) == 0xFFFFFFFFu) continue;
+    const uint64_t wp = pv[w >> 32];
+    // a resolved target passes its value on; otherwise skip to its parent
+    pv[i] = (wp >> 32) == 0xFFFFFFFFu ? wp : (wp & 0xFFFFFFFF00000000ull);
+    changed = true;
+  }
+  if (__any_sync(0xffffffffu, changed) && (threadIdx.x & 31) == 0) *flag = 1;
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) k_up_targets(State<T> s, const uint32_t* __restrict__ up,
+                                                    uint32_t nup, int fam,
+                                                    const uint64_t* __restrict__ pv,
+                                                    uint32_t* __restrict__ targets) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint32_t* fL = fam ? s.fm : s.fM;
+  uint32_t mism = 0;
+  for (uint64_t wb = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) & ~uint64_t(31);
+       wb < nup; wb += stride) {
+    const uint64_t i = wb + (threadIdx.x & 31);
+    bool hit = false;
+    uint32_t t = 0;
+    if (i < nup) {
+      const uint32_t v = up[i];
+      const uint32_t fc = (__ldg(s.fdir + v) >> (4 * fam)) & 15u;
+      const uint32_t gc = (__ldg(s.gdir + v) >> (4 * fam)) & 15u;
+      if (gc != fc && static_cast<uint32_t>(pv[i]) != __ldg(fL + v)) {  // divergent, mismatched
+        ++mism;
+        const uint32_t c = fam ? fc : gc;  // desc lowers f's step, asc g's step
+        if (c == kSelf) atomicExch(&s.ctl->status, kStatusTroubleMax);
+        t = c == kSelf ? v : v + s.geo.off[c];
+        hit = true;
+      }
+    }
+    warp_append(hit, t, targets, &s.ctl->list_count[0]);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mism += __shfl_xor_sync(0xffffffffu, mism, o);
@@ -1104,6 +1520,25 @@ __device__ __forceinline__ uint32_t false_cp_bytes(uint32_t f, uint32_t g) {
   const uint32_t fmx = zero_bytes(~f & 0x0F0F0F0Fu), gmx = zero_bytes(~g & 0x0F0F0F0Fu);
   const uint32_t fmn = zero_bytes(~f & 0xF0F0F0F0u), gmn = zero_bytes(~g & 0xF0F0F0F0u);
   return (fmx ^ gmx) | (fmn ^ gmn);
+}
+
+// Gate restricted to the vertices whose codes an R batch may have changed
+// (the frontier list F of k_frontier): before the batch there were none.
+__global__ void __launch_bounds__(256) k_count_false_list(const uint8_t* __restrict__ fdir,
+                                                          const uint8_t* __restrict__ gdir,
+                                                          const uint32_t* __restrict__ F,
+                                                          const uint32_t* nF, uint64_t* total) {
+  const uint32_t n = *nF;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  uint32_t c = 0;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint32_t u = F[i];
+    c += __popc(false_cp_bytes(fdir[u], gdir[u]) & 0xFFu);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c)
+    atomicAdd(reinterpret_cast<unsigned long long*>(total), static_cast<unsigned long long>(c));
 }
 
 __global__ void __launch_bounds__(256) k_count_false(const uint8_t* __restrict__ fdir,
