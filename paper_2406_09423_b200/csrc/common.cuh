@@ -252,6 +252,25 @@ __device__ __forceinline__ void warp_append_cap(bool pred, uint32_t val, uint32_
   if (pred && pos < cap) list[pos] = val;
 }
 
+// Per-lane staging buffer (in the warp's shared-memory slice `st`, K x 32
+// words) for list appends inside warp-uniform loops: values are written with
+// ONE warp reservation when some lane's buffer is full (and at the end)
+// instead of one contended global atomic per loop iteration.  All calls must
+// be made by the full warp.
+template <int K>
+struct WarpBuffer {
+  uint32_t* st;  // st[j * 32 + lane]
+  int n = 0;
+  __device__ __forceinline__ explicit WarpBuffer(uint32_t* stage) : st(stage) {}
+  __device__ __forceinline__ void flush(uint32_t* __restrict__ list, uint32_t* count);
+  __device__ __forceinline__ void push(bool pred, uint32_t val, uint32_t* __restrict__ list,
+                                       uint32_t* count) {
+    if (__any_sync(0xffffffffu, n == K)) flush(list, count);
+    if (pred) st[n * 32 + (threadIdx.x & 31)] = val;
+    n += pred ? 1 : 0;
+  }
+};
+
 // Per-lane count c -> returns this lane's slot base after a single warp atomic.
 __device__ __forceinline__ uint32_t warp_reserve(uint32_t c, uint32_t* count) {
   const int lane = threadIdx.x & 31;
@@ -266,6 +285,22 @@ __device__ __forceinline__ uint32_t warp_reserve(uint32_t c, uint32_t* count) {
   if (lane == 31 && total) base = atomicAdd(count, total);
   base = __shfl_sync(0xffffffffu, base, 31);
   return base + incl - c;
+}
+
+template <int K>
+__device__ __forceinline__ void WarpBuffer<K>::flush(uint32_t* __restrict__ list, uint32_t* count) {
+  __syncwarp();
+  const uint32_t pos = warp_reserve(static_cast<uint32_t>(n), count);
+  for (int j = 0; j < n; ++j) list[pos + j] = st[j * 32 + (threadIdx.x & 31)];
+  __syncwarp();
+  n = 0;
+}
+
+constexpr int kStageK = 4;
+constexpr int kStageWarps = 16;  // blocks of up to 512 threads
+// per-warp staging slice of a [kStageWarps][kStageK * 32] shared array
+__device__ __forceinline__ uint32_t* warp_stage(uint32_t (*arr)[kStageK * 32]) {
+  return arr[threadIdx.x >> 5];
 }
 
 }  // namespace mssz_b200

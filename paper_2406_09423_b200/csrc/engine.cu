@@ -703,9 +703,14 @@ struct Engine {
     if (c.status == kStatusStall)
       fail(MSSZ_CU_ERR_NON_CONVERGENCE, "%s subloop stalled at the float floor", kKindName[kind]);
     if (trace)
-      std::fprintf(stderr, "[mssz] C kind=%d iters=%llu edits=%llu big=%llu frontier=%llu\n", kind,
-                   (unsigned long long)c.iters, (unsigned long long)c.edits,
-                   (unsigned long long)c.big_batches, (unsigned long long)c.frontier);
+      std::fprintf(stderr,
+                   "[mssz] C kind=%d iters=%llu edits=%llu big=%llu frontier=%llu small_ms=%.2f big_ms=%.2f\n",
+                   kind, (unsigned long long)c.iters, (unsigned long long)c.edits,
+                   (unsigned long long)c.big_batches, (unsigned long long)c.frontier,
+                   c.small_ns * 1e-6, c.big_ns * 1e-6);
+    if (trace && c.big_batches)
+      std::fprintf(stderr, "[mssz]   big phases fix=%.2f frontier=%.2f rebuild=%.2f ms\n",
+                   c.phase_ns[0] * 1e-6, c.phase_ns[1] * 1e-6, c.phase_ns[2] * 1e-6);
     st.sub_iterations[kind] += c.iters;
     st.effective_edits += c.edits;
     st.frontier_vertices += c.frontier;

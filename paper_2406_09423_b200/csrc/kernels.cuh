@@ -34,6 +34,10 @@ struct Ctl {
   uint32_t cmd_it;
   uint32_t pad_;
   uint64_t big_batches;  // batches that ran grid-wide
+  uint64_t small_ns, big_ns;  // k_subloop batch time by regime (%globaltimer, leader thread)
+  uint64_t phase_ns[3];       // big batches: fix / frontier / rebuild
+  uint32_t retry_count;       // k_subloop: old-list items whose target was not lowered
+  uint32_t pad2_;
   uint32_t sp_count[4];  // sparse R-loop: X / frontier (2) / Up sizes
   uint32_t sp_abort;
   uint32_t sp_levels;
@@ -408,12 +412,19 @@ __device__ __forceinline__ bool claim_and_lower(const State<T>& s, uint32_t t, u
   return true;
 }
 
+// retry (optional): list items whose target this item did not lower itself
+// (claim lost, or target at its floor).  Every other item is a neighbour of
+// (or is) a lowered target, hence in this batch's frontier, and is
+// re-evaluated there; only retry items need the old-list membership test.
 template <class T>
 __device__ __forceinline__ void fix_batch(const State<T>& s, const uint32_t* __restrict__ list,
                                           uint32_t n, int rule, uint32_t batch, uint32_t* s_count,
-                                          uint64_t tid, uint64_t stride) {
+                                          uint64_t tid, uint64_t stride, uint32_t* retry = nullptr,
+                                          uint32_t* retry_count = nullptr) {
   // two list items per lane per step: their loads and claims overlap
   const uint64_t step = 2 * stride;
+  __shared__ uint32_t sstage[kStageWarps][kStageK * 32], rstage[kStageWarps][kStageK * 32];
+  WarpBuffer<kStageK> sbuf(warp_stage(sstage)), rbuf(warp_stage(rstage));
   for (uint64_t wb = (tid & ~uint64_t(31)) * 2; wb < n; wb += step) {
     const uint64_t i0 = wb + (threadIdx.x & 31), i1 = i0 + 32;
     uint32_t t[2] = {0, 0};
@@ -449,9 +460,15 @@ __device__ __forceinline__ void fix_batch(const State<T>& s, const uint32_t* __r
         ok[j] = true;
       }
     }
-    warp_append(ok[0], t[0], s.S, s_count);
-    warp_append(ok[1], t[1], s.S, s_count);
+    sbuf.push(ok[0], t[0], s.S, s_count);
+    sbuf.push(ok[1], t[1], s.S, s_count);
+    if (retry) {
+      rbuf.push(live[0] && !ok[0], v[0], retry, retry_count);
+      rbuf.push(live[1] && !ok[1], v[1], retry, retry_count);
+    }
   }
+  sbuf.flush(s.S, s_count);
+  if (retry) rbuf.flush(retry, retry_count);
 }
 
 // Stencil slot k -> (dx, dy, dz) without tables: slots come in (+d, -d) pairs
@@ -475,15 +492,23 @@ __device__ __forceinline__ void slot_delta(int k, int& dx, int& dy, int& dz) {
 // One lane per (edited vertex, candidate slot): 16 lanes per vertex in 3D
 // (self + 14 slots), 8 in 2D, so every lane has one claim and one direction
 // evaluation in flight instead of a serial chain of 15.
+// next (optional, C-loop): instead of collecting F, append every frontier
+// vertex that is of `kind` under its refreshed code straight to the next
+// worklist (f_count then only counts the frontier).
 template <class T, int DIM>
 __device__ __forceinline__ void frontier_update(const State<T>& s, uint32_t ns, uint32_t mark,
-                                                uint32_t* f_count, uint64_t tid, uint64_t stride) {
+                                                uint32_t* f_count, uint64_t tid, uint64_t stride,
+                                                int kind = -1, uint32_t* next = nullptr,
+                                                uint32_t* next_count = nullptr) {
   constexpr int LPS = DIM == 2 ? 8 : 16;  // lanes per edited vertex
   constexpr int NS = StencilSize<DIM>::value;
   const uint64_t total = static_cast<uint64_t>(ns) * LPS;
+  __shared__ uint32_t nstage[kStageWarps][kStageK * 32];
+  WarpBuffer<kStageK> nbuf(warp_stage(nstage));
+  uint32_t nmine = 0;
   for (uint64_t wb = tid & ~uint64_t(31); wb < total; wb += stride) {
     const uint64_t i = wb + (threadIdx.x & 31);
-    bool mine = false;
+    bool mine = false, keep = false;
     uint32_t u = 0;
     if (i < total) {
       const int k = static_cast<int>(i % LPS) - 1;  // -1 = the edited vertex itself
@@ -500,6 +525,7 @@ __device__ __forceinline__ void frontier_update(const State<T>& s, uint32_t ns, 
             mine = true;
             const uint8_t code =
                 static_cast<uint8_t>(direction_code<T, DIM, true>(s.g, s.geo, u, ux, uy, uz));
+            if (next) keep = kind_match(kind, __ldg(s.fdir + u), code);
             if (s.gdir[u] != code) {
               s.gdir[u] = code;
               if (s.tdirty) s.tdirty[label_tile_of<DIM>(s.geo, ux, uy, uz)] = 1;
@@ -512,28 +538,36 @@ __device__ __forceinline__ void frontier_update(const State<T>& s, uint32_t ns, 
         }
       }
     }
-    warp_append(mine, u, s.F, f_count);
+    if (next) {
+      nbuf.push(keep, u, next, next_count);
+      nmine += mine ? 1u : 0u;
+    } else {
+      warp_append(mine, u, s.F, f_count);
+    }
+  }
+  if (next) {
+    nbuf.flush(next, next_count);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nmine += __shfl_xor_sync(0xffffffffu, nmine, o);
+    if ((threadIdx.x & 31) == 0 && nmine) atomicAdd(f_count, nmine);
   }
 }
 
-// New worklist = (old list minus frontier) ∪ {u in frontier : kind(u)}.
+// New worklist = (old list minus frontier) ∪ {u in frontier : kind(u)}.  The
+// second part is appended by frontier_update; here only the retry items
+// (the old-list entries that can lie outside the frontier) are checked.
 // Exact: only frontier vertices can change class after a batch.
-template <class T>
-__device__ __forceinline__ void rebuild_list(const State<T>& s, int kind, const uint32_t* old,
-                                             uint32_t nold, uint32_t* nxt, uint32_t* nxt_count,
-                                             uint32_t nf, uint32_t mark, uint64_t tid,
-                                             uint64_t stride) {
-  const uint64_t total = static_cast<uint64_t>(nf) + nold;
-  for (uint64_t wb = tid & ~uint64_t(31); wb < total; wb += stride) {
+__device__ __forceinline__ void rebuild_retry(const uint32_t* __restrict__ retry, uint32_t nr,
+                                              const uint32_t* __restrict__ fmark, uint32_t mark,
+                                              uint32_t* nxt, uint32_t* nxt_count, uint64_t tid,
+                                              uint64_t stride) {
+  for (uint64_t wb = tid & ~uint64_t(31); wb < nr; wb += stride) {
     const uint64_t i = wb + (threadIdx.x & 31);
     bool keep = false;
     uint32_t v = 0;
-    if (i < nf) {
-      v = __ldcg(s.F + i);
-      keep = kind_match(kind, __ldg(s.fdir + v), __ldcg(s.gdir + v));
-    } else if (i < total) {
-      v = __ldcg(old + (i - nf));
-      keep = __ldcg(s.fmark + v) != mark;
+    if (i < nr) {
+      v = __ldcg(retry + i);
+      keep = __ldcg(fmark + v) != mark;
     }
     warp_append(keep, v, nxt, nxt_count);
   }
@@ -640,25 +674,44 @@ __device__ BatchResult big_batch(const State<T>& s, cg::grid_group& grid, int ki
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   const int rule = (kind == 0 || kind == 3) ? 0 : 1;
   const uint32_t batch = batch_base + 2 * it, mark = mark_base + it;
-  fix_batch(s, s.list[cur], n, rule, batch, &ctl->s_count, tid, stride);
+  uint64_t t0 = 0, t1 = 0, t2 = 0;
+  if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  fix_batch(s, s.list[cur], n, rule, batch, &ctl->s_count, tid, stride, s.F, &ctl->retry_count);
   grid.sync();
   uint32_t applied = *reinterpret_cast<volatile uint32_t*>(&ctl->s_count);
   if (applied == 0 && kind == 1) {
     grid.sync();  // every thread has read applied == 0 before the fallback appends to S
-    fix_batch(s, s.list[cur], n, 2, batch + 1, &ctl->s_count, tid, stride);
+    if (tid == 0) ctl->retry_count = 0;
+    grid.sync();
+    fix_batch(s, s.list[cur], n, 2, batch + 1, &ctl->s_count, tid, stride, s.F, &ctl->retry_count);
     grid.sync();
     applied = *reinterpret_cast<volatile uint32_t*>(&ctl->s_count);
   }
   if (applied == 0) return {0, 0};
-  frontier_update<T, DIM>(s, applied, mark, &ctl->f_count, tid, stride);
+  if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+  // frontier size only feeds EditStats: count it per CTA in shared memory
+  __shared__ uint32_t block_frontier;
+  if (threadIdx.x == 0) block_frontier = 0;
+  __syncthreads();
+  frontier_update<T, DIM>(s, applied, mark, &block_frontier, tid, stride, kind, s.list[cur ^ 1],
+                          &ctl->list_count[cur ^ 1]);
+  __syncthreads();
+  if (threadIdx.x == 0 && block_frontier) atomicAdd(&ctl->f_count, block_frontier);
   grid.sync();
+  if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
   const uint32_t nf = *reinterpret_cast<volatile uint32_t*>(&ctl->f_count);
-  rebuild_list(s, kind, s.list[cur], n, s.list[cur ^ 1], &ctl->list_count[cur ^ 1], nf, mark, tid,
-               stride);
+  const uint32_t nr = *reinterpret_cast<volatile uint32_t*>(&ctl->retry_count);
+  rebuild_retry(s.F, nr, s.fmark, mark, s.list[cur ^ 1], &ctl->list_count[cur ^ 1], tid, stride);
   grid.sync();
   if (tid == 0) {
+    uint64_t t3;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t3));
+    ctl->phase_ns[0] += t1 - t0;
+    ctl->phase_ns[1] += t2 - t1;
+    ctl->phase_ns[2] += t3 - t2;
     ctl->s_count = 0;
     ctl->f_count = 0;
+    ctl->retry_count = 0;
     ctl->list_count[cur] = 0;
   }
   return {applied, nf};
@@ -667,29 +720,32 @@ __device__ BatchResult big_batch(const State<T>& s, cg::grid_group& grid, int ki
 template <class T, int DIM>
 __device__ BatchResult small_batch(const State<T>& s, int kind, uint32_t n, uint32_t cur,
                                    uint32_t it, uint32_t batch_base, uint32_t mark_base,
-                                   uint32_t* cnt /* smem [3] */) {
+                                   uint32_t* cnt /* smem [4] */) {
   const uint64_t tid = threadIdx.x, stride = blockDim.x;
   const int rule = (kind == 0 || kind == 3) ? 0 : 1;
   const uint32_t batch = batch_base + 2 * it, mark = mark_base + it;
-  fix_batch(s, s.list[cur], n, rule, batch, &cnt[0], tid, stride);
+  fix_batch(s, s.list[cur], n, rule, batch, &cnt[0], tid, stride, s.F, &cnt[3]);
   __syncthreads();
   uint32_t applied = *reinterpret_cast<volatile uint32_t*>(&cnt[0]);
   if (applied == 0 && kind == 1) {
     __syncthreads();
-    fix_batch(s, s.list[cur], n, 2, batch + 1, &cnt[0], tid, stride);
+    if (threadIdx.x == 0) cnt[3] = 0;
+    __syncthreads();
+    fix_batch(s, s.list[cur], n, 2, batch + 1, &cnt[0], tid, stride, s.F, &cnt[3]);
     __syncthreads();
     applied = *reinterpret_cast<volatile uint32_t*>(&cnt[0]);
   }
   if (applied == 0) return {0, 0};
-  frontier_update<T, DIM>(s, applied, mark, &cnt[1], tid, stride);
+  frontier_update<T, DIM>(s, applied, mark, &cnt[1], tid, stride, kind, s.list[cur ^ 1], &cnt[2]);
   __syncthreads();
   const uint32_t nf = *reinterpret_cast<volatile uint32_t*>(&cnt[1]);
-  rebuild_list(s, kind, s.list[cur], n, s.list[cur ^ 1], &cnt[2], nf, mark, tid, stride);
+  const uint32_t nr = *reinterpret_cast<volatile uint32_t*>(&cnt[3]);
+  rebuild_retry(s.F, nr, s.fmark, mark, s.list[cur ^ 1], &cnt[2], tid, stride);
   __syncthreads();
   if (threadIdx.x == 0) {
     s.ctl->list_count[cur ^ 1] = cnt[2];
     s.ctl->list_count[cur] = 0;
-    cnt[0] = cnt[1] = cnt[2] = 0;
+    cnt[0] = cnt[1] = cnt[2] = cnt[3] = 0;
   }
   __syncthreads();
   return {applied, nf};
@@ -702,8 +758,8 @@ __global__ void __launch_bounds__(kSubThreads, 2)
   cg::grid_group grid = cg::this_grid();
   Ctl* ctl = s.ctl;
   __shared__ uint32_t cmd[4];
-  __shared__ uint32_t cnt[3];
-  if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
+  __shared__ uint32_t cnt[4];
+  if (threadIdx.x < 4) cnt[threadIdx.x] = 0;
   __syncthreads();
 
   if (blockIdx.x != 0) {  // worker CTAs: join broadcast batches
@@ -731,7 +787,7 @@ __global__ void __launch_bounds__(kSubThreads, 2)
 
   uint32_t cur = *reinterpret_cast<volatile uint32_t*>(&ctl->cur);
   uint64_t attempted = *reinterpret_cast<volatile uint64_t*>(&ctl->attempted);
-  uint64_t iters = 0, edits = 0, frontier = 0, big = 0;
+  uint64_t iters = 0, edits = 0, frontier = 0, big = 0, small_ns = 0, big_ns = 0;
   uint32_t status = kStatusOk, done = 0, seq = 0;
   for (;;) {
     const uint32_t n = *reinterpret_cast<volatile uint32_t*>(&ctl->list_count[cur]);
@@ -747,8 +803,15 @@ __global__ void __launch_bounds__(kSubThreads, 2)
     }
     const uint32_t it = static_cast<uint32_t>(attempted);
     BatchResult r;
+    uint64_t t0 = 0;
+    if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     if (n <= small_max) {
       r = small_batch<T, DIM>(s, kind, n, cur, it, batch_base, mark_base, cnt);
+      if (threadIdx.x == 0) {
+        uint64_t t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        small_ns += t1 - t0;
+      }
     } else {
       if (threadIdx.x == 0) {
         ctl->cmd_type = kCmdBatch;
@@ -761,6 +824,11 @@ __global__ void __launch_bounds__(kSubThreads, 2)
       r = big_batch<T, DIM>(s, grid, kind, n, cur, it, batch_base, mark_base);
       ++big;
       __syncthreads();
+      if (threadIdx.x == 0) {
+        uint64_t t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        big_ns += t1 - t0;
+      }
     }
     if (r.applied == 0) {
       status = kStatusStall;
@@ -785,6 +853,8 @@ __global__ void __launch_bounds__(kSubThreads, 2)
     ctl->edits += edits;
     ctl->frontier += frontier;
     ctl->big_batches += big;
+    ctl->small_ns += small_ns;
+    ctl->big_ns += big_ns;
     ctl->status = status;
   }
 }
