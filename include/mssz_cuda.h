@@ -173,6 +173,56 @@ int mssz_cu_classify_critical(uint64_t n, const uint64_t* asc, const uint64_t* d
                               uint64_t* maxima, uint64_t* n_max, uint64_t* minima,
                               uint64_t* n_min);
 
+/* ---- z-slab sharding ----------------------------------------
+ * A 3D field is split along axis 2 into P contiguous slabs of >= 2 planes
+ * (slab r owns planes [floor(Z r/P), floor(Z (r+1)/P))).  Each rank passes its
+ * WINDOW: the owned planes plus up to two halo planes per side, i.e. planes
+ * [wz0, wz1) of mssz_cu_slab_range().  The edits a rank returns are the ones in
+ * its owned planes, as GLOBAL ids, sorted; concatenated in rank order they are
+ * the EditSet of derive_edits (edit_engine.cpp:368-378) on the whole field, and
+ * the result -- edits, values and EditStats -- is identical to the
+ * single-device engine's.  Global vertex counts must be < 2^32 - 1.
+ *
+ * One process per GPU: rank 0 calls mssz_cu_comm_unique_id and broadcasts the
+ * id (e.g. torch.distributed), then every rank calls mssz_cu_comm_init
+ * (NCCL: all-gathers of per-batch status records and boundary label tables,
+ * send/recv of boundary edits with the z neighbours). */
+#define MSSZ_CU_UNIQUE_ID_BYTES 128
+typedef struct mssz_cu_comm mssz_cu_comm;
+
+/* out = {z0, z1, wz0, wz1}: owned planes [z0, z1), window planes [wz0, wz1). */
+int mssz_cu_slab_range(uint64_t Z, int nranks, int rank, uint64_t out[4]);
+int mssz_cu_comm_unique_id(uint8_t* id /* MSSZ_CU_UNIQUE_ID_BYTES */);
+int mssz_cu_comm_init(const uint8_t* id, int nranks, int rank, int device, mssz_cu_comm** out);
+int mssz_cu_comm_destroy(mssz_cu_comm* comm);
+
+/* _slab: host window in, this slab's part of the EditSet out (offset_out = its
+ *   position in the global EditSet); stats are global (identical on every rank).
+ * _slab_device: same, device-resident window and outputs, ordered after cuda_stream.
+ * _slabs_local: nslabs virtual ranks in this process (host threads on
+ *   devices[r % ndevices], or the current device); whole-field host buffers in,
+ *   whole EditSet out (single-GPU testing of the sharded schedule). */
+#define MSSZ_CU_DECLARE_SLAB(SUF, T)                                                              \
+  int mssz_cu_derive_edits_slab_##SUF(mssz_cu_comm* comm, int ndims, const uint64_t* dims,       \
+                                      const T* original_window, const T* decompressed_window,   \
+                                      double xi, const mssz_cu_options* opt, uint64_t* indices, \
+                                      T* values, uint64_t capacity, uint64_t* count_out,        \
+                                      uint64_t* offset_out, mssz_cu_stats* stats_out);          \
+  int mssz_cu_derive_edits_slab_device_##SUF(                                                    \
+      mssz_cu_comm* comm, int ndims, const uint64_t* dims, const T* d_original_window,           \
+      const T* d_decompressed_window, double xi, const mssz_cu_options* opt, uint64_t* d_indices, \
+      T* d_values, uint64_t capacity, uint64_t* count_out, uint64_t* offset_out,                 \
+      mssz_cu_stats* stats_out, void* cuda_stream);                                              \
+  int mssz_cu_derive_edits_slabs_local_##SUF(int nslabs, const int* devices, int ndevices,      \
+                                             int ndims, const uint64_t* dims, const T* original, \
+                                             const T* decompressed, double xi,                   \
+                                             const mssz_cu_options* opt, uint64_t* indices,      \
+                                             T* values, uint64_t capacity, uint64_t* count_out,  \
+                                             mssz_cu_stats* stats_out);
+
+MSSZ_CU_DECLARE_SLAB(f32, float)
+MSSZ_CU_DECLARE_SLAB(f64, double)
+
 #ifdef __cplusplus
 }
 #endif

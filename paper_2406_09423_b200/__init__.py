@@ -32,7 +32,7 @@ __all__ = [
     "derive_edits", "derive_edits_into", "derive_edits_device", "compute_directions",
     "compute_direction_codes", "compute_labels", "classify_critical", "detect_false_critical",
     "detect_kind", "lower_step", "representable_floor", "apply_edits", "segmentation_equal",
-    "library", "build",
+    "library", "build", "slab_range", "derive_edits_slabs", "SlabComm",
 ]
 
 FPMAX, FPMIN, FNMAX, FNMIN = 0, 1, 2, 3
@@ -270,21 +270,38 @@ _BATCH_CB = C.CFUNCTYPE(None, C.c_void_p, C.c_uint64, C.c_void_p)
 EXPORTS = [
     "mssz_cu_default_options", "mssz_cu_last_error", "mssz_cu_free", "mssz_cu_device_count",
     "mssz_cu_version", "mssz_cu_release_workspace", "mssz_cu_compute_labels",
-    "mssz_cu_classify_critical",
+    "mssz_cu_classify_critical", "mssz_cu_slab_range", "mssz_cu_comm_unique_id",
+    "mssz_cu_comm_init", "mssz_cu_comm_destroy",
 ] + [
     f"mssz_cu_{name}_{suf}" for suf in ("f32", "f64") for name in (
         "derive_edits", "derive_edits_into", "derive_edits_device", "compute_directions",
         "compute_direction_codes", "detect_false_critical", "detect_kind", "lower_step",
-        "representable_floor", "apply_edits")
+        "representable_floor", "apply_edits", "derive_edits_slab", "derive_edits_slab_device",
+        "derive_edits_slabs_local")
 ]
 
 _lib = None
+
+
+def _nccl_path() -> Optional[str]:
+    """torch's bundled libnccl.so.2 (nvidia-nccl wheel), if installed."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for base in (spec.submodule_search_locations or []) if spec else []:
+        cand = os.path.join(base, "nccl", "lib", "libnccl.so.2")
+        if os.path.exists(cand):
+            return cand
+    return None
 
 
 def library() -> C.CDLL:
     """Loads ``_lib/libmssz_b200.so`` (fails loudly when it has not been built)."""
     global _lib
     if _lib is None:
+        if "MSSZ_NCCL_LIBRARY" not in os.environ:
+            path = _nccl_path()
+            if path:
+                os.environ["MSSZ_NCCL_LIBRARY"] = path
         if not os.path.exists(CUDA_SO):
             raise Error(ErrKind.cuda, f"CUDA extension missing: {CUDA_SO} (run build())")
         lib = C.CDLL(CUDA_SO)
@@ -514,3 +531,113 @@ def segmentation_equal(a: SegmentationLabels, b: SegmentationLabels):
         raise Error(ErrKind.usage, "segmentation_equal: topology mismatch")
     match = (a.max_label == b.max_label) & (a.min_label == b.min_label)
     return match.astype(np.uint8), int(match.size - int(match.sum()))
+
+
+# ---------------------------------------------------------------- z-slab sharding
+def slab_range(z_extent: int, nranks: int, rank: int) -> tuple:
+    """(z0, z1, wz0, wz1): owned planes [z0, z1) and window planes [wz0, wz1) of a rank."""
+    out = (C.c_uint64 * 4)()
+    _check(library().mssz_cu_slab_range(C.c_uint64(z_extent), nranks, rank, out))
+    return tuple(int(v) for v in out)
+
+
+def derive_edits_slabs(topo: GridTopology, original, decompressed, xi: float, nslabs: int,
+                       opts: Optional[DeriveOptions] = None, stats: Optional[EditStats] = None,
+                       devices=None) -> EditSet:
+    """derive_edits on ``nslabs`` z-slabs run as virtual ranks in this process
+    (host threads; all on ``opts.device`` unless ``devices`` is given).  The
+    result equals derive_edits on the whole field (the sharding acceptance
+    test)."""
+    f = _field(topo, original, "original")
+    fh = _field(topo, decompressed, "decompressed", f.dtype)
+    suf = _suf(f.dtype)
+    keep: list = []
+    co = _options(opts, f.dtype, keep)
+    cap = topo.vertex_count
+    idx = np.empty(cap, np.uint64)
+    val = np.empty(cap, f.dtype)
+    count = C.c_uint64()
+    st = _Stats()
+    devs = None if not devices else (C.c_int * len(devices))(*devices)
+    rc = getattr(library(), f"mssz_cu_derive_edits_slabs_local_{suf}")(
+        nslabs, devs, len(devices) if devices else 0, topo.ndims, _dims(topo), _p(f), _p(fh),
+        C.c_double(xi), C.byref(co), _p(idx), _p(val), C.c_uint64(cap), C.byref(count),
+        C.byref(st))
+    _check(rc)
+    if stats is not None:
+        st.fill(stats)
+    k = count.value
+    return EditSet(idx[:k].copy(), val[:k].copy())
+
+
+class SlabComm:
+    """One rank of a z-slab sharded run (one process per GPU, NCCL underneath).
+
+    ``SlabComm.unique_id()`` on rank 0, broadcast (e.g. torch.distributed), then
+    ``SlabComm(uid, nranks, rank, device)`` everywhere.  ``derive_edits`` takes
+    this rank's window (planes ``slab_range(...)[2:4]``) and returns the edits in
+    its owned planes (global ids) plus their offset in the global EditSet."""
+
+    def __init__(self, uid: bytes, nranks: int, rank: int, device: int):
+        if len(uid) != 128:
+            raise Error(ErrKind.usage, "NCCL unique id must be 128 bytes")
+        self.nranks, self.rank, self.device = nranks, rank, device
+        self._c = C.c_void_p()
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        _check(library().mssz_cu_comm_init(buf, nranks, rank, device, C.byref(self._c)))
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        _check(library().mssz_cu_comm_unique_id(buf))
+        return bytes(buf)
+
+    def close(self) -> None:
+        if self._c:
+            _check(library().mssz_cu_comm_destroy(self._c))
+            self._c = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def derive_edits(self, dims, original_window, decompressed_window, xi: float,
+                     opts: Optional[DeriveOptions] = None, stats: Optional[EditStats] = None):
+        """-> (EditSet of this slab, offset in the global EditSet)."""
+        f = np.ascontiguousarray(original_window).reshape(-1)
+        fh = np.ascontiguousarray(decompressed_window, dtype=f.dtype).reshape(-1)
+        z0, z1, wz0, wz1 = slab_range(int(dims[2]), self.nranks, self.rank)
+        want = int(dims[0]) * int(dims[1]) * (wz1 - wz0)
+        if f.size != want or fh.size != want:
+            raise Error(ErrKind.io, f"window holds {f.size} values, expected {want}")
+        keep: list = []
+        co = _options(opts, f.dtype, keep)
+        cap = int(dims[0]) * int(dims[1]) * (z1 - z0)
+        idx = np.empty(cap, np.uint64)
+        val = np.empty(cap, f.dtype)
+        count, offset, st = C.c_uint64(), C.c_uint64(), _Stats()
+        rc = getattr(library(), f"mssz_cu_derive_edits_slab_{_suf(f.dtype)}")(
+            self._c, 3, (C.c_uint64 * 3)(*[int(d) for d in dims]), _p(f), _p(fh), C.c_double(xi),
+            C.byref(co), _p(idx), _p(val), C.c_uint64(cap), C.byref(count), C.byref(offset),
+            C.byref(st))
+        _check(rc)
+        if stats is not None:
+            st.fill(stats)
+        k = count.value
+        return EditSet(idx[:k].copy(), val[:k].copy()), offset.value
+
+    def derive_edits_device(self, dims, d_f: int, d_fh: int, xi: float, d_idx: int, d_val: int,
+                            capacity: int, dtype=np.float32, opts: Optional[DeriveOptions] = None,
+                            stream: int = 0) -> tuple:
+        """Device-resident window -> (count, offset, EditStats)."""
+        keep: list = []
+        co = _options(opts, dtype, keep)
+        count, offset, st = C.c_uint64(), C.c_uint64(), _Stats()
+        rc = getattr(library(), f"mssz_cu_derive_edits_slab_device_{_suf(dtype)}")(
+            self._c, 3, (C.c_uint64 * 3)(*[int(d) for d in dims]), C.c_void_p(d_f), C.c_void_p(d_fh),
+            C.c_double(xi), C.byref(co), C.c_void_p(d_idx), C.c_void_p(d_val), C.c_uint64(capacity),
+            C.byref(count), C.byref(offset), C.byref(st), C.c_void_p(stream or None))
+        _check(rc)
+        return count.value, offset.value, st.fill(EditStats())

@@ -179,6 +179,20 @@ struct Workspace {
     CK(cudaFuncSetAttribute(k_label_tile<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(label_tile_smem<3>())));
   }
+  // private workspaces (virtual slab ranks) free everything, not just buffers
+  void destroy() {
+    release();
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : pev) cudaEventDestroy(e);
+    pev.clear();
+    if (ctl) cudaFree(ctl);
+    if (hctl) cudaFreeHost(hctl);
+    if (stream) cudaStreamDestroy(stream);
+    ctl = nullptr;
+    hctl = nullptr;
+    stream = nullptr;
+  }
   void release() {
     for (DevBuf* b : {&f, &g, &fdir, &gdir, &touched, &stamp, &fmark, &lab, &fin, &lists, &tiles,
                       &tE, &tEcnt, &toldfin, &tdirty, &taffected, &tbits, &tcnt, &tlist, &xbuf, &cbits})
@@ -328,6 +342,8 @@ struct Engine {
     s.ctl = ws.ctl;
     s.tdirty = nullptr;
     s.cdirty = ws.cbits.as<uint32_t>();
+    s.own_lo = s.act_lo = 0;
+    s.own_n = s.act_n = geo.n;
   }
 
   // Per-kernel-class device time (CUDA events on the launching stream), only
@@ -1020,7 +1036,8 @@ struct Engine {
   }
 
   // edits() (edit_engine.cpp:368-378) into device buffers; returns the count.
-  uint64_t compact(const uint8_t* flag, uint8_t want, const T* vals, uint64_t* d_idx, T* d_val) {
+  uint64_t compact(const uint8_t* flag, uint8_t want, const T* vals, uint64_t* d_idx, T* d_val,
+                   uint64_t base = 0) {
     const uint64_t ntiles = (static_cast<uint64_t>(n()) + kCompactTile - 1) / kCompactTile;
     uint32_t* tiles = ws.tiles.as<uint32_t>();
     pre(kProfCompact);
@@ -1031,7 +1048,7 @@ struct Engine {
     launched(kProfCompact);
     pre(kProfCompact);
     k_compact_write<T><<<static_cast<uint32_t>(ntiles), kCompactThreads, 0, ws.stream>>>(
-        flag, n(), want, vals, tiles, d_idx, d_val);
+        flag, n(), want, vals, tiles, d_idx, d_val, base);
     launched(kProfCompact);
     uint64_t total = 0;
     CK(cudaMemcpyAsync(&total, &ws.ctl->mism, sizeof total, cudaMemcpyDeviceToHost, ws.stream));
@@ -1522,3 +1539,5 @@ int mssz_cu_classify_critical(uint64_t n, const uint64_t* asc, const uint64_t* d
 }
 
 }  // extern "C"
+
+#include "shard_api.cuh"

@@ -41,6 +41,7 @@ struct Ctl {
   uint32_t sp_count[4];  // sparse R-loop: X / frontier (2) / Up sizes
   uint32_t sp_abort;
   uint32_t sp_levels;
+  uint32_t bnd[2];       // z-slab sharding: boundary edits packed for rank-1 / rank+1
 };
 
 enum : uint32_t {
@@ -397,6 +398,10 @@ struct State {
   Ctl* ctl;
   uint8_t* tdirty;  // R-loop only: label tiles whose direction codes changed
   uint32_t* cdirty; // 1 bit per 64-vertex chunk whose codes changed (sparse R pass's X)
+  // z-slab sharding (shard.cuh): fixes lower only targets in [own_lo, own_lo + own_n),
+  // frontier refreshes only vertices in [act_lo, act_lo + act_n) (owned planes plus
+  // one halo plane per side).  Single device: both ranges are the whole grid.
+  uint32_t own_lo, own_n, act_lo, act_n;
 };
 
 // claim (edit_engine.cpp:160-169) + lower_step (:75-86): the first claimant of
@@ -441,8 +446,8 @@ __device__ __forceinline__ void fix_batch(const State<T>& s, const uint32_t* __r
     }
     uint32_t prev[2] = {batch, batch};
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
-      if (live[j]) prev[j] = atomicExch(&s.stamp[t[j]], batch);
+    for (int j = 0; j < 2; ++j)  // only the owner of a target lowers it (owner-computes)
+      if (live[j] && t[j] - s.own_lo < s.own_n) prev[j] = atomicExch(&s.stamp[t[j]], batch);
     T gv[2], fv[2];
 #pragma unroll
     for (int j = 0; j < 2; ++j)
@@ -519,8 +524,8 @@ __device__ __forceinline__ void frontier_update(const State<T>& s, uint32_t ns, 
         int dx = 0, dy = 0, dz = 0;
         if (k >= 0) slot_delta<DIM>(k, dx, dy, dz);
         const uint32_t ux = x + dx, uy = y + dy, uz = z + dz;
-        if (ux < s.geo.X && uy < s.geo.Y && (DIM == 2 || uz < s.geo.Z)) {
-          u = ux + s.geo.X * uy + s.geo.XY * uz;
+        if (ux < s.geo.X && uy < s.geo.Y && (DIM == 2 || uz < s.geo.Z) &&
+            (u = ux + s.geo.X * uy + s.geo.XY * uz) - s.act_lo < s.act_n) {
           if (__ldcg(s.fmark + u) != mark && atomicExch(&s.fmark[u], mark) != mark) {
             mine = true;
             const uint8_t code =
@@ -1751,7 +1756,7 @@ template <class T>
 __global__ void __launch_bounds__(kCompactThreads) k_compact_write(
     const uint8_t* __restrict__ flag, uint64_t n, uint8_t want, const T* __restrict__ g,
     const uint32_t* __restrict__ tile_offsets, uint64_t* __restrict__ idx_out,
-    T* __restrict__ val_out) {
+    T* __restrict__ val_out, uint64_t base) {
   __shared__ uint32_t wsum[kCompactThreads / 32];
   const uint64_t v0 = (static_cast<uint64_t>(blockIdx.x) * kCompactThreads + threadIdx.x) * kCompactPer;
   uint32_t bits = v0 < n ? tile_flags(flag, n, v0, want) : 0u;
@@ -1771,7 +1776,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_write(
   while (bits) {
     const int j = __ffs(bits) - 1;
     bits &= bits - 1;
-    idx_out[pos] = v0 + j;
+    idx_out[pos] = base + v0 + j;  // base: global id of the first slab vertex
     if (val_out) val_out[pos] = g[v0 + j];
     ++pos;
   }
