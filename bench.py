@@ -18,8 +18,12 @@ postconditions → EditSet compaction) over one synthetic field.
 * cpu_baseline — the UNMODIFIED reference (oracle/_ref/libmssz_ref.so,
            OpenMP, all host cores) on a bounded sample of the same workload.
 
-N > 1 (torchrun): every rank corrects its own replica of the field (weak
-scaling; z-slab sharding of one field is the next multi-GPU step).
+N > 1 (torchrun), 3D configs: the field is z-slab sharded, one slab per rank
+(SURVEY §8(e), strong scaling: the total field is fixed).  Rank 0 generates the
+field and sends every rank its window (owned planes + 2 halo planes per side)
+over NCCL before timing; each step is one sharded derive_edits through
+mssz_cu_derive_edits_slab_device (value) / mssz_cu_derive_edits_slab (e2e).
+2D configs at N > 1 run one replica per rank (weak scaling).
 """
 from __future__ import annotations
 
@@ -74,6 +78,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--cpu-dims", default=None)
+    ap.add_argument("--shard", action="store_true",
+                    help="z-slab sharded path even at N=1 (one-rank NCCL communicator)")
     return ap.parse_args()
 
 
@@ -250,13 +256,46 @@ def main():
     n = topo.vertex_count
 
     t_gen = time.perf_counter()
-    f, fh, xi = I.make_inputs(cfg, dims, dtype)
+    sharded = (dist.world > 1 or args.shard) and len(dims) == 3
+    if sharded and dist.rank != 0:
+        f = fh = xi = None  # sharded: rank 0 generates and sends the windows
+    else:
+        f, fh, xi = I.make_inputs(cfg, dims, dtype)
     t_gen = time.perf_counter() - t_gen
 
     dev = torch.device("cuda", dist.local)
-    df = torch.from_numpy(f).to(dev)
-    dfh = torch.from_numpy(fh).to(dev)
-    cap = n
+    comm = None
+    if sharded:
+        # rank 0 holds the whole field; every rank receives its window over NCCL
+        XY = dims[0] * dims[1]
+        z0, z1, wz0, wz1 = P.slab_range(dims[2], dist.world, dist.rank)
+        meta = [xi, P.SlabComm.unique_id() if dist.rank == 0 else None]
+        if dist.pg:
+            dist.pg.broadcast_object_list(meta, src=0)
+        xi = meta[0]
+        if dist.rank == 0:
+            full = [torch.from_numpy(a).to(dev) for a in (f, fh)]
+            for r in range(1, dist.world):
+                _, _, a, b = P.slab_range(dims[2], dist.world, r)
+                for t in full:
+                    dist.pg.send(t[a * XY:b * XY].contiguous(), dst=r)
+            df, dfh = (t[wz0 * XY:wz1 * XY].clone() for t in full)
+            del full
+        else:
+            df = torch.empty((wz1 - wz0) * XY, dtype=tdtype, device=dev)
+            dfh = torch.empty_like(df)
+            for t in (df, dfh):
+                dist.pg.recv(t, src=0)
+        torch.cuda.synchronize()
+        f = fh = None  # host copies of the window are made for the e2e leg below
+        comm = P.SlabComm(meta[1], dist.world, dist.rank, dist.local)
+        cap = (z1 - z0) * XY
+        n_local = df.numel()
+    else:
+        df = torch.from_numpy(f).to(dev)
+        dfh = torch.from_numpy(fh).to(dev)
+        cap = n
+        n_local = n
     d_idx = torch.empty(cap, dtype=torch.int64, device=dev)
     d_val = torch.empty(cap, dtype=tdtype, device=dev)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
@@ -265,6 +304,11 @@ def main():
                            profile=not args.no_profile)
 
     def step():
+        if comm is not None:
+            c, _, s = comm.derive_edits_device(dims, df.data_ptr(), dfh.data_ptr(), xi,
+                                               d_idx.data_ptr(), d_val.data_ptr(), cap, dtype,
+                                               opts, stream.cuda_stream)
+            return c, s
         return P.derive_edits_device(topo, df.data_ptr(), dfh.data_ptr(), xi, d_idx.data_ptr(),
                                      d_val.data_ptr(), cap, dtype, opts, stream.cuda_stream)
 
@@ -290,7 +334,7 @@ def main():
     dist.barrier()
     clk = clocks.stop()
     ms = dist.max(statistics.mean(step_ms))
-    total_vertices = dist.sum(float(n))
+    total_vertices = float(n) if sharded else dist.sum(float(n))
     value = total_vertices / (ms * 1e-3) / 1e6
 
     # ---- roofline of the dominant kernel class (live, from the timed steps)
@@ -308,7 +352,7 @@ def main():
         graded = {k: v for k, v in agg.items() if alg_bytes_per_vertex(k, es) and v["launches"]}
         top = max(graded, key=lambda k: graded[k]["ms"])
         per_launch_ms = graded[top]["ms"] / graded[top]["launches"]
-        bytes_per_launch = alg_bytes_per_vertex(top, es) * n
+        bytes_per_launch = alg_bytes_per_vertex(top, es) * n_local
         achieved = bytes_per_launch / (per_launch_ms * 1e-3) / 1e9
         total_ms = sum(v["ms"] for v in agg.values())
         roofline = {"kernel": top, "bound": "hbm", "achieved": achieved, "peak": peak,
@@ -321,26 +365,38 @@ def main():
     # ---- e2e through the host API with pinned buffers
     e2e = None
     if not args.no_e2e:
-        hf = torch.from_numpy(f).pin_memory()
-        hfh = torch.from_numpy(fh).pin_memory()
+        hf = (df.cpu() if sharded else torch.from_numpy(f)).pin_memory()
+        hfh = (dfh.cpu() if sharded else torch.from_numpy(fh)).pin_memory()
         h_idx = torch.empty(max(count, 1), dtype=torch.int64).pin_memory()
         h_val = torch.empty(max(count, 1), dtype=tdtype).pin_memory()
         e2e_opts = P.DeriveOptions(subloop_cap=cfg.subloop_cap, device=dist.local)
-        P.derive_edits_into(topo, hf.data_ptr(), hfh.data_ptr(), xi, h_idx.data_ptr(),
-                            h_val.data_ptr(), h_idx.numel(), dtype, e2e_opts)
+
+        def host_step():
+            if comm is not None:
+                c, _, _ = comm.derive_edits_into(dims, hf.data_ptr(), hfh.data_ptr(), xi,
+                                                 h_idx.data_ptr(), h_val.data_ptr(),
+                                                 h_idx.numel(), dtype, e2e_opts)
+                return c
+            c, _ = P.derive_edits_into(topo, hf.data_ptr(), hfh.data_ptr(), xi, h_idx.data_ptr(),
+                                       h_val.data_ptr(), h_idx.numel(), dtype, e2e_opts)
+            return c
+
+        host_step()
         walls = []
         dist.barrier()
         for _ in range(args.steps):
             flush.fill_(1.0)
             torch.cuda.synchronize()
             t = time.perf_counter()
-            c2, _ = P.derive_edits_into(topo, hf.data_ptr(), hfh.data_ptr(), xi, h_idx.data_ptr(),
-                                        h_val.data_ptr(), h_idx.numel(), dtype, e2e_opts)
+            c2 = host_step()
             walls.append(time.perf_counter() - t)
         wall = dist.max(statistics.mean(walls))
+        api = ("mssz_cu_derive_edits_slab (pinned host windows)" if sharded
+               else "mssz_cu_derive_edits_into (pinned host buffers)")
         e2e = {"value": total_vertices / wall / 1e6, "unit": UNIT,
-               "h2d_bytes_per_step": 2 * n * es, "d2h_bytes_per_step": int(c2) * (8 + es),
-               "ms_per_step": wall * 1e3, "api": "mssz_cu_derive_edits_into (pinned host buffers)"}
+               "h2d_bytes_per_step": int(dist.sum(2.0 * n_local * es)),
+               "d2h_bytes_per_step": int(dist.sum(float(c2) * (8 + es))),
+               "ms_per_step": wall * 1e3, "api": api}
 
     # ---- CPU baseline: the unmodified reference on a bounded sample (rank 0, N=1)
     cpu = None
@@ -364,17 +420,18 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": args.dtype, "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
         "config": {"workload": cfg.note, "dims": list(dims), "vertices": n, "kind": cfg.kind,
                    "rel_eb": cfg.rel, "xi": xi, "subloop_cap": cfg.subloop_cap,
-                   "parallelism": f"replica-per-gpu x{dist.world}",
+                   "parallelism": (f"z-slab x{dist.world} (NCCL)" if sharded
+                                   else f"replica-per-gpu x{dist.world}"),
                    "l2": "flushed between steps (512 MB write outside the timed events)",
                    "input_gen_s": round(t_gen, 2)},
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": int(sum(s.kernel_launches for s in stats)),
+        "gpu_launches": int(dist.sum(float(sum(s.kernel_launches for s in stats)))),
         "clocks": clk,
         "edit_stats": {"outer_iterations": st.outer_iterations, "c_passes": st.c_passes,
                        "sub_iterations": st.sub_iterations, "r_iterations": st.r_iterations,
@@ -387,6 +444,8 @@ def main():
     }
     if dist.rank == 0:
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     dist.done()
 
 

@@ -628,6 +628,20 @@ class SlabComm:
         k = count.value
         return EditSet(idx[:k].copy(), val[:k].copy()), offset.value
 
+    def derive_edits_into(self, dims, f_ptr: int, fh_ptr: int, xi: float, idx_ptr: int,
+                          val_ptr: int, capacity: int, dtype=np.float32,
+                          opts: Optional[DeriveOptions] = None) -> tuple:
+        """Host-pointer window (e.g. pinned) -> (count, offset, EditStats)."""
+        keep: list = []
+        co = _options(opts, dtype, keep)
+        count, offset, st = C.c_uint64(), C.c_uint64(), _Stats()
+        rc = getattr(library(), f"mssz_cu_derive_edits_slab_{_suf(dtype)}")(
+            self._c, 3, (C.c_uint64 * 3)(*[int(d) for d in dims]), C.c_void_p(f_ptr),
+            C.c_void_p(fh_ptr), C.c_double(xi), C.byref(co), C.c_void_p(idx_ptr),
+            C.c_void_p(val_ptr), C.c_uint64(capacity), C.byref(count), C.byref(offset), C.byref(st))
+        _check(rc)
+        return count.value, offset.value, st.fill(EditStats())
+
     def derive_edits_device(self, dims, d_f: int, d_fh: int, xi: float, d_idx: int, d_val: int,
                             capacity: int, dtype=np.float32, opts: Optional[DeriveOptions] = None,
                             stream: int = 0) -> tuple:

@@ -279,10 +279,13 @@ __global__ void __launch_bounds__(256) k_mask_dir(const uint8_t* __restrict__ di
   }
 }
 
-// Provisional labels of the first / last owned plane -> this rank's table part
-// [family][side][xy] (global ids).
+// Window labels of the first / last owned plane -> this rank's table part
+// [family][side][xy] (global ids).  Label = fin[prov[v]] (label_pass without
+// its finish phase: prov is a root or a resolved exit).
 __global__ void __launch_bounds__(256) k_publish_labels(const uint32_t* __restrict__ M,
-                                                        const uint32_t* __restrict__ m, uint32_t XY,
+                                                        const uint32_t* __restrict__ m,
+                                                        const uint32_t* __restrict__ finM,
+                                                        const uint32_t* __restrict__ finm, uint32_t XY,
                                                         uint32_t own_lo, uint32_t own_hi, uint32_t base,
                                                         uint32_t* __restrict__ tab) {
   const uint64_t total = 4ull * XY;
@@ -292,7 +295,7 @@ __global__ void __launch_bounds__(256) k_publish_labels(const uint32_t* __restri
     const int side = static_cast<int>((i / XY) & 1);
     const uint32_t xy = static_cast<uint32_t>(i % XY);
     const uint32_t v = side ? own_hi - XY + xy : own_lo + xy;
-    tab[i] = (fam ? m[v] : M[v]) + base;
+    tab[i] = (fam ? finm[m[v]] : finM[M[v]]) + base;
   }
 }
 
@@ -329,13 +332,15 @@ __global__ void __launch_bounds__(256) k_resolve_table(uint32_t* __restrict__ ta
 // table entry when it lies on a boundary plane (halo vertices: their own entry).
 __global__ void __launch_bounds__(256) k_final_labels(const uint32_t* __restrict__ M,
                                                       const uint32_t* __restrict__ m,
+                                                      const uint32_t* __restrict__ finM,
+                                                      const uint32_t* __restrict__ finm,
                                                       const uint32_t* __restrict__ tab, SlabTable t,
                                                       uint32_t lo, uint32_t hi, uint32_t base,
                                                       int resolve, uint32_t* __restrict__ FM,
                                                       uint32_t* __restrict__ Fm) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t v = lo + static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < hi; v += stride) {
-    uint32_t a = M[v] + base, d = m[v] + base;
+    uint32_t a = finM[M[v]] + base, d = finm[m[v]] + base;
     if (resolve) {
       const int64_t sa = table_slot(t, a, 0), sd = table_slot(t, d, 1);
       if (sa >= 0) a = __ldg(tab + sa);
@@ -346,13 +351,30 @@ __global__ void __launch_bounds__(256) k_final_labels(const uint32_t* __restrict
   }
 }
 
+// Final global g label of a window vertex from its provisional label.
+__device__ __forceinline__ uint32_t g_final(const uint32_t* __restrict__ prov, const uint32_t* __restrict__ fin,
+                                            const uint32_t* __restrict__ tab, const SlabTable& t,
+                                            uint32_t base, int resolve, uint32_t v, int fam) {
+  uint32_t L = __ldg(fin + __ldg(prov + v)) + base;
+  if (resolve) {
+    const int64_t sl = table_slot(t, L, fam);
+    if (sl >= 0) L = __ldg(tab + sl);
+  }
+  return L;
+}
+
 // R batch targets over the active range (see k_rfix_tiles for the walk-free
 // argument; find_troublemaker, edit_engine.cpp:293-315): a divergent vertex w
 // whose final label differs contributes g-asc(w) / f-desc(w).  Targets are
 // kept by their owner only; mismatches are counted on owned vertices only.
+// g labels are resolved only for divergent vertices (no full finish pass).
 template <class T>
-__global__ void __launch_bounds__(256) k_slab_rtargets(State<T> s, const uint32_t* __restrict__ gFM,
-                                                       const uint32_t* __restrict__ gFm,
+__global__ void __launch_bounds__(256) k_slab_rtargets(State<T> s, const uint32_t* __restrict__ gM,
+                                                       const uint32_t* __restrict__ gm,
+                                                       const uint32_t* __restrict__ finM,
+                                                       const uint32_t* __restrict__ finm,
+                                                       const uint32_t* __restrict__ tab, SlabTable tb,
+                                                       uint32_t base, int resolve,
                                                        uint32_t* __restrict__ targets, uint32_t* count) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   const uint64_t hi = static_cast<uint64_t>(s.act_lo) + s.act_n;
@@ -365,8 +387,10 @@ __global__ void __launch_bounds__(256) k_slab_rtargets(State<T> s, const uint32_
     if (v < hi) {
       const uint32_t fc = __ldg(s.fdir + v), gc = __ldg(s.gdir + v);
       const bool owned = v - s.own_lo < s.own_n;
-      const bool ma = (gc & 15u) != (fc & 15u) && __ldg(gFM + v) != __ldg(s.fM + v);
-      const bool md = (gc >> 4) != (fc >> 4) && __ldg(gFm + v) != __ldg(s.fm + v);
+      const bool ma = (gc & 15u) != (fc & 15u) &&
+                      g_final(gM, finM, tab, tb, base, resolve, v, 0) != __ldg(s.fM + v);
+      const bool md = (gc >> 4) != (fc >> 4) &&
+                      g_final(gm, finm, tab, tb, base, resolve, v, 1) != __ldg(s.fm + v);
       if (owned) mism += (ma ? 1u : 0u) + (md ? 1u : 0u);
       if (ma) {
         const uint32_t c = gc & 15u;
@@ -594,10 +618,10 @@ SlabPlan slab_plan(uint64_t Z, int P, int r) {
 
 // Workspace extras of the sharded loop.
 struct SlabBufs {
-  DevBuf ldir, tab_mine, tab_all, send[2], recv[2], rec, rec_all, gfin;
+  DevBuf ldir, tab_mine, tab_all, send[2], recv[2], rec, rec_all;
   std::vector<Rec> hrec;
   void release() {
-    for (DevBuf* b : {&ldir, &tab_mine, &tab_all, &send[0], &send[1], &recv[0], &recv[1], &rec, &rec_all, &gfin})
+    for (DevBuf* b : {&ldir, &tab_mine, &tab_all, &send[0], &send[1], &recv[0], &recv[1], &rec, &rec_all})
       b->release();
   }
 };
@@ -630,7 +654,6 @@ struct SlabEngine {
     for (uint32_t r = 0; r <= pl.P; ++r) stab.z0[r] = static_cast<uint32_t>(uint64_t(pl.Z) * r / pl.P);
     const size_t nw = eng.n();
     sb.ldir.ensure(nw + 16);
-    sb.gfin.ensure(size_t((nw + 63) & ~size_t(63)) * 8);
     sb.tab_mine.ensure(size_t(4) * XY * 4);
     sb.tab_all.ensure(size_t(4) * XY * 4 * pl.P);
     for (int k = 0; k < 2; ++k) {
@@ -645,8 +668,6 @@ struct SlabEngine {
   uint32_t n() const { return eng.n(); }
   mssz_cu_stats& st() { return eng.st; }
   State<T>& s() { return eng.s; }
-  uint32_t* gFM() const { return sb.gfin.as<uint32_t>(); }
-  uint32_t* gFm() const { return sb.gfin.as<uint32_t>() + ((eng.n() + 63) & ~63u); }
   uint32_t blocks(uint64_t work, int per_sm = 8) const { return grid_for(work, 256, ws.sms, per_sm); }
 
   // all-gathered status records of every rank (blocking)
@@ -705,18 +726,21 @@ struct SlabEngine {
   }
 
   // ---- labels of one direction field (f at setup, g per R iteration) ----
-  void labels(const uint8_t* dir, uint32_t* FM, uint32_t* Fm) {
+  // Window labels with the off-slab vertices masked as extrema, then the
+  // boundary tables.  finals: also write final global labels of the active
+  // range to FM / Fm (f); otherwise (g) k_slab_rtargets resolves them lazily.
+  void labels(const uint8_t* dir, uint32_t* FM, uint32_t* Fm, bool finals) {
     eng.pre(kProfLabelInit);
     k_mask_dir<<<blocks(n() / 16 + 1, 16), 256, 0, ws.stream>>>(dir, n(), own_lo, own_hi, sb.ldir.as<uint8_t>());
     eng.launched(kProfLabelInit);
     uint32_t* M = eng.lab(2);
     uint32_t* m = eng.lab(3);
-    eng.label_pass(sb.ldir.as<uint8_t>(), M, m, /*only_dirty=*/false, /*finish=*/true);
+    eng.label_pass(sb.ldir.as<uint8_t>(), M, m, /*only_dirty=*/false, /*finish=*/false);
     const bool multi = pl.P > 1;
     if (multi) {
       eng.pre(kProfLabelJump);
-      k_publish_labels<<<blocks(4ull * XY), 256, 0, ws.stream>>>(M, m, XY, own_lo, own_hi, base,
-                                                                  sb.tab_mine.as<uint32_t>());
+      k_publish_labels<<<blocks(4ull * XY), 256, 0, ws.stream>>>(M, m, eng.fin(0), eng.fin(1), XY, own_lo,
+                                                                  own_hi, base, sb.tab_mine.as<uint32_t>());
       eng.launched(kProfLabelJump);
       tr.allgather_dev(sb.tab_mine.p, sb.tab_all.p, size_t(4) * XY * 4, ws.stream);
       CK(cudaMemsetAsync(&ws.ctl->sp_abort, 0, 4, ws.stream));
@@ -725,9 +749,11 @@ struct SlabEngine {
                                                                             &ws.ctl->sp_abort);
       eng.launched(kProfLabelJump);
     }
+    if (!finals) return;
     eng.pre(kProfLabelFinish);
     k_final_labels<<<blocks(act_hi - act_lo, 16), 256, 0, ws.stream>>>(
-        M, m, sb.tab_all.as<uint32_t>(), stab, act_lo, act_hi, base, multi ? 1 : 0, FM, Fm);
+        M, m, eng.fin(0), eng.fin(1), sb.tab_all.as<uint32_t>(), stab, act_lo, act_hi, base, multi ? 1 : 0,
+        FM, Fm);
     eng.launched(kProfLabelFinish);
   }
 
@@ -833,17 +859,17 @@ struct SlabEngine {
 
   // g labels + R targets + (speculative) fix; returns the global mismatch count
   uint64_t r_batch(uint32_t batch) {
-    labels(s().gdir, gFM(), gFm());
+    labels(s().gdir, nullptr, nullptr, false);
     // label_pass used list_count[0] as a scratch counter
     CK(cudaMemsetAsync(&ws.ctl->list_count[0], 0, sizeof(uint32_t), ws.stream));
     CK(cudaMemsetAsync(&ws.ctl->mism, 0, sizeof(uint64_t), ws.stream));
     CK(cudaMemsetAsync(&ws.ctl->status, 0, sizeof(uint32_t), ws.stream));
     eng.pre(kProfRfix);
-    k_slab_rtargets<T><<<blocks(act_hi - act_lo, 16), 256, 0, ws.stream>>>(s(), gFM(), gFm(), eng.list(0),
-                                                                            &ws.ctl->list_count[0]);
+    k_slab_rtargets<T><<<blocks(act_hi - act_lo, 16), 256, 0, ws.stream>>>(
+        s(), eng.lab(2), eng.lab(3), eng.fin(0), eng.fin(1), sb.tab_all.as<uint32_t>(), stab, base,
+        pl.P > 1 ? 1 : 0, eng.list(0), &ws.ctl->list_count[0]);
     eng.launched(kProfRfix);
     fix(0, batch, eng.list(0), &ws.ctl->list_count[0], false);
-    ++st().label_passes;
     gather();
     if (sum([](const Rec& r) { return r.err; }))
       fail(MSSZ_CU_ERR_INTERNAL, "path compression exceeded its round cap (corrupt direction field)");
@@ -916,8 +942,7 @@ struct SlabEngine {
     eng.directions(d_f, ws.fdir.as<uint8_t>());
     eng.directions(S.g, S.gdir);
     CK(cudaEventRecord(ws.ev[1], ws.stream));
-    labels(S.fdir, eng.lab(0), eng.lab(1));
-    ++st().label_passes;
+    labels(S.fdir, eng.lab(0), eng.lab(1), true);
     gather();
     if (sum([](const Rec& r) { return r.err; }))
       fail(MSSZ_CU_ERR_INTERNAL, "path compression exceeded its round cap (corrupt direction field)");
