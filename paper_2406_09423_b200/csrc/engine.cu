@@ -178,6 +178,10 @@ struct Workspace {
                             static_cast<int>(label_tile_smem<2>())));
     CK(cudaFuncSetAttribute(k_label_tile<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(label_tile_smem<3>())));
+    CK(cudaFuncSetAttribute(k_directions_reg3<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(sizeof(D3Smem))));
+    CK(cudaFuncSetAttribute(k_directions_reg3<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(sizeof(D3Smem))));
   }
   // private workspaces (virtual slab ranks) free everything, not just buffers
   void destroy() {
@@ -388,6 +392,19 @@ struct Engine {
       chunk = std::min<uint32_t>(chunk, 64);
       dim3 grid(bx, (geo.Y + chunk - 1) / chunk);
       k_directions_tiled<T, 2><<<grid, DT::BX * DT::BY, 0, ws.stream>>>(vals, dir, geo, chunk);
+    } else if (sizeof(T) == 4) {
+      const uint32_t bx = (geo.X + kD3W - 1) / kD3W, by = (geo.Y + kD3H - 1) / kD3H;
+      const uint64_t tiles = uint64_t(bx) * by;
+      // >= ~4 waves of 2 CTAs/SM, chunks of >= 8 planes
+      uint32_t zc = static_cast<uint32_t>(std::min<uint64_t>(
+          std::max<uint64_t>(1, (uint64_t(ws.sms) * 8 + tiles - 1) / tiles), std::max<uint32_t>(1, geo.Z / 8)));
+      const uint32_t chunk = (geo.Z + zc - 1) / zc;
+      dim3 grid(bx, by, (geo.Z + chunk - 1) / chunk);
+      const float* fv = reinterpret_cast<const float*>(vals);
+      if (geo.X % 4 == 0)
+        k_directions_reg3<true, 2><<<grid, kD3Warps * 32, sizeof(D3Smem), ws.stream>>>(fv, dir, geo, chunk);
+      else
+        k_directions_reg3<false, 2><<<grid, kD3Warps * 32, sizeof(D3Smem), ws.stream>>>(fv, dir, geo, chunk);
     } else {
       using DB = DirBlock3<T>;
       const uint32_t bx = (geo.X + DB::BX - 1) / DB::BX, by = (geo.Y + DB::BY - 1) / DB::BY;

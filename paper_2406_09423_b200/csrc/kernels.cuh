@@ -324,6 +324,247 @@ __global__ void __launch_bounds__(DirBlock3<T>::BX * DirBlock3<T>::BY)
   }
 }
 
+// K1 (3D, f32, register-blocked).  Same decomposition as k_directions_block3,
+// restructured so per-vertex work is a handful of compares:
+//  * a warp owns one grid row of a 128-wide tile, each lane 4 consecutive x
+//    (one 16-byte load and one 4-byte store per lane per plane); warps 1..H
+//    are output rows, warp 0 the halo row above (cells only), warp H+1 the
+//    halo row below (keys only);
+//  * cell(x,y,z) = the 2x2 block {x,x+1} x {y,y+1} of plane z, extremes with
+//    their position (SoS: >= keeps the later index for ascending, < the
+//    earlier for descending);
+//  * the A pair of vertex (x,y,z) is VA(x,y,z) = [cell(x,y,z), cell(x,y,z+1)];
+//    its C pair [cell(x-1,y-1,z-1), cell(x-1,y-1,z)] is VA(x-1,y-1,z-1), so
+//    each pair is reduced once by its own thread and read once by the vertex
+//    at (x+1, y+1, z+1) through shared memory;
+//  * one barrier per plane: keys of plane p+1 and VA of plane p-1 are
+//    published while plane p-1's vertices read VA of plane p-2 (2 key slots,
+//    3 VA slots).
+// Keys: order-preserving u32 (x + 0.0f maps -0 to +0: SoS ties them); cells
+// outside the grid hold key 0, which never wins ascending (key) nor
+// descending (key - 1 wraps to ~0).
+constexpr int kD3W = 128, kD3H = 14, kD3Warps = kD3H + 2, kD3P = 136;
+
+__device__ __forceinline__ uint32_t fkey(float x) {
+  const uint32_t b = __float_as_uint(x + 0.0f);
+  return b ^ (static_cast<uint32_t>(static_cast<int32_t>(b) >> 31) | 0x80000000u);
+}
+
+// 2x2 cell extremes; corners in index order c0 (x,y) c1 (x+1,y) c2 (x,y+1) c3 (x+1,y+1).
+// pos = ascending corner | descending corner << 2
+__device__ __forceinline__ void cell_ext(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t& a,
+                                         uint32_t& d, uint32_t& pos) {
+  uint32_t hp = 0, lp = 0;
+  a = c0;
+  if (c1 >= a) { a = c1; hp = 1; }
+  if (c2 >= a) { a = c2; hp = 2; }
+  if (c3 >= a) { a = c3; hp = 3; }
+  d = c0 - 1;
+  if (c1 - 1 < d) { d = c1 - 1; lp = 1; }
+  if (c2 - 1 < d) { d = c2 - 1; lp = 2; }
+  if (c3 - 1 < d) { d = c3 - 1; lp = 3; }
+  pos = hp | (lp << 2);
+}
+
+// pair [lower plane, upper plane] of cells: pos byte = asc (0..7) | desc (0..7) << 4
+__device__ __forceinline__ void pair_ext(uint32_t a0, uint32_t d0, uint32_t p0, uint32_t a1, uint32_t d1,
+                                         uint32_t p1, uint32_t& a, uint32_t& d, uint32_t& pos) {
+  uint32_t hp = p0 & 3u, lp = p0 >> 2;
+  a = a0;
+  d = d0;
+  if (a1 >= a) { a = a1; hp = 4 + (p1 & 3u); }
+  if (d1 < d) { d = d1; lp = 4 + (p1 >> 2); }
+  pos = hp | (lp << 4);
+}
+
+struct D3Smem {
+  uint32_t skey[2][kD3Warps][kD3P];  // keys per row (column x at x - x0 + 4)
+  uint32_t sva[2][kD3H + 1][kD3P];   // VA ascending keys per cell row
+  uint32_t svd[2][kD3H + 1][kD3P];   // VA descending keys
+  uint8_t svp[2][kD3H + 1][kD3P];    // VA positions
+};
+
+// per-thread constants of k_directions_reg3
+struct D3Ctx {
+  const float* vals;
+  uint8_t* dir;
+  int64_t XY, rowbase;
+  int lane, w, x0, xl, c, X, Z, s1;
+  bool row_in, cells, out;
+};
+
+// state carried from plane p-1 to plane p
+struct D3State {
+  uint4 k;                    // this row's keys of plane p
+  uint32_t kh;                // halo key of plane p (lane 0: x0-1, lane 31: x0+128)
+  uint32_t ca[5], cd[5], cp;  // cells of plane p-1 (own 4 + lane 0's x0-1), positions 4 bits each
+};
+
+template <bool kVec>
+__device__ __forceinline__ void d3_load(const D3Ctx& t, int z, float4& v, float& h) {
+  v = make_float4(0.f, 0.f, 0.f, 0.f);
+  h = 0.f;
+  if (!t.row_in || z < 0 || z >= t.Z) return;
+  const float* base = t.vals + t.XY * z + t.rowbase;
+  if (kVec) {
+    if (t.xl < t.X) v = __ldg(reinterpret_cast<const float4*>(base + t.xl));
+  } else {
+    if (t.xl < t.X) v.x = __ldg(base + t.xl);
+    if (t.xl + 1 < t.X) v.y = __ldg(base + t.xl + 1);
+    if (t.xl + 2 < t.X) v.z = __ldg(base + t.xl + 2);
+    if (t.xl + 3 < t.X) v.w = __ldg(base + t.xl + 3);
+  }
+  if (t.lane == 0 && t.x0 > 0) h = __ldg(base + t.x0 - 1);
+  if (t.lane == 31 && t.x0 + kD3W < t.X) h = __ldg(base + t.x0 + kD3W);
+}
+
+__device__ __forceinline__ void d3_keys(const D3Ctx& t, int z, const float4& v, float h, uint4& k, uint32_t& kh) {
+  const bool zin = t.row_in && z >= 0 && z < t.Z;
+  k.x = (zin && t.xl < t.X) ? fkey(v.x) : 0u;
+  k.y = (zin && t.xl + 1 < t.X) ? fkey(v.y) : 0u;
+  k.z = (zin && t.xl + 2 < t.X) ? fkey(v.z) : 0u;
+  k.w = (zin && t.xl + 3 < t.X) ? fkey(v.w) : 0u;
+  const bool hin = zin && ((t.lane == 0 && t.x0 > 0) || (t.lane == 31 && t.x0 + kD3W < t.X));
+  kh = hin ? fkey(h) : 0u;
+}
+
+__device__ __forceinline__ void d3_publish(const D3Ctx& t, uint32_t (*sk)[kD3P], const uint4& k, uint32_t kh) {
+  *reinterpret_cast<uint4*>(&sk[t.w][t.c]) = k;
+  if (t.lane == 0) sk[t.w][3] = kh;
+  if (t.lane == 31) sk[t.w][kD3W + 4] = kh;
+}
+
+// One plane step (see k_directions_reg3).  PAR = parity of the step: keys of
+// plane p sit in key slot PAR, VA(p-1) goes to VA slot PAR, VA(p-2) is read
+// from slot PAR ^ 1.  pv/ph hold plane p+1's values on entry and receive
+// plane p+3's on exit.
+template <int PAR, bool kVec>
+__device__ __forceinline__ void d3_step(const D3Ctx& t, D3Smem& S, int p, int s0, const D3State& in,
+                                        D3State& o, float4& pv, float& ph) {
+  // 1. keys of plane p+1 -> key slot PAR^1
+  d3_keys(t, p + 1, pv, ph, o.k, o.kh);
+  d3_publish(t, S.skey[PAR ^ 1], o.k, o.kh);
+  d3_load<kVec>(t, p + 3, pv, ph);
+  // 2. cells of plane p: rows y (in.k) and y+1 (smem)
+  o.cp = 0;
+  if (t.cells) {
+    const uint32_t* below = S.skey[PAR][t.w + 1];
+    const uint4 b = *reinterpret_cast<const uint4*>(below + t.c);
+    const uint32_t b4 = below[t.c + 4];
+    uint32_t a4 = __shfl_down_sync(0xffffffffu, in.k.x, 1);
+    if (t.lane == 31) a4 = in.kh;
+    uint32_t q;
+    cell_ext(in.k.x, in.k.y, b.x, b.y, o.ca[0], o.cd[0], q);
+    o.cp = q;
+    cell_ext(in.k.y, in.k.z, b.y, b.z, o.ca[1], o.cd[1], q);
+    o.cp |= q << 4;
+    cell_ext(in.k.z, in.k.w, b.z, b.w, o.ca[2], o.cd[2], q);
+    o.cp |= q << 8;
+    cell_ext(in.k.w, a4, b.w, b4, o.ca[3], o.cd[3], q);
+    o.cp |= q << 12;
+    o.ca[4] = 0;
+    o.cd[4] = ~0u;
+    if (t.lane == 0) {
+      cell_ext(in.kh, in.k.x, below[3], b.x, o.ca[4], o.cd[4], q);
+      o.cp |= q << 16;
+    }
+  }
+  if (p < s0 || !t.cells) return;
+  // 3. VA(p-1) = [cell(p-1), cell(p)] -> VA slot PAR
+  uint32_t va[4], vd[4], vpk = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint32_t q;
+    pair_ext(in.ca[i], in.cd[i], (in.cp >> (4 * i)) & 15u, o.ca[i], o.cd[i], (o.cp >> (4 * i)) & 15u, va[i],
+             vd[i], q);
+    vpk |= q << (8 * i);
+  }
+  *reinterpret_cast<uint4*>(&S.sva[PAR][t.w][t.c]) = make_uint4(va[0], va[1], va[2], va[3]);
+  *reinterpret_cast<uint4*>(&S.svd[PAR][t.w][t.c]) = make_uint4(vd[0], vd[1], vd[2], vd[3]);
+  *reinterpret_cast<uint32_t*>(&S.svp[PAR][t.w][t.c]) = vpk;
+  if (t.lane == 0) {
+    uint32_t ea, ed, ep;
+    pair_ext(in.ca[4], in.cd[4], (in.cp >> 16) & 15u, o.ca[4], o.cd[4], (o.cp >> 16) & 15u, ea, ed, ep);
+    S.sva[PAR][t.w][3] = ea;
+    S.svd[PAR][t.w][3] = ed;
+    S.svp[PAR][t.w][3] = static_cast<uint8_t>(ep);
+  }
+  // 4. vertices of plane p-1: C pair = VA(x-1, y-1, p-2) (slot PAR^1), A pair = own VA(p-1)
+  if (p < s0 + 1 || p - 1 >= t.s1 || !t.out) return;
+  const uint32_t* ra = S.sva[PAR ^ 1][t.w - 1];
+  const uint32_t* rd = S.svd[PAR ^ 1][t.w - 1];
+  const uint8_t* rp = S.svp[PAR ^ 1][t.w - 1];
+  const uint4 qa = *reinterpret_cast<const uint4*>(ra + t.c);
+  const uint4 qd = *reinterpret_cast<const uint4*>(rd + t.c);
+  const uint32_t Cpk = (*reinterpret_cast<const uint32_t*>(rp + t.c) << 8) | rp[t.c - 1];
+  const uint32_t Ca[4] = {ra[t.c - 1], qa.x, qa.y, qa.z};
+  const uint32_t Cd[4] = {rd[t.c - 1], qd.x, qd.y, qd.z};
+  uint32_t codes = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t cpi = (Cpk >> (8 * i)) & 0xFFu, vpi = (vpk >> (8 * i)) & 0xFFu;
+    const uint32_t hi = va[i] >= Ca[i] ? 8 + (vpi & 15u) : (cpi & 15u);
+    const uint32_t lo = vd[i] < Cd[i] ? 8 + (vpi >> 4) : (cpi >> 4);
+    const uint32_t hc = static_cast<uint32_t>(kBlockSlot3 >> (4 * hi)) & 15u;
+    const uint32_t lc = static_cast<uint32_t>(kBlockSlot3 >> (4 * lo)) & 15u;
+    codes |= (hc | (lc << 4)) << (8 * i);
+  }
+  uint8_t* op = t.dir + t.XY * (p - 1) + t.rowbase + t.xl;
+  if (kVec) {
+    if (t.xl < t.X) *reinterpret_cast<uint32_t*>(op) = codes;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (t.xl + i < t.X) op[i] = static_cast<uint8_t>(codes >> (8 * i));
+  }
+}
+
+template <bool kVec, int kMinBlocks>
+__global__ void __launch_bounds__(kD3Warps * 32, kMinBlocks)
+    k_directions_reg3(const float* __restrict__ vals, uint8_t* __restrict__ dir, Geom g, int chunk) {
+  extern __shared__ __align__(16) unsigned char d3raw[];
+  D3Smem& S = *reinterpret_cast<D3Smem*>(d3raw);
+  D3Ctx t;
+  t.vals = vals;
+  t.dir = dir;
+  t.lane = threadIdx.x & 31;
+  t.w = threadIdx.x >> 5;
+  t.x0 = blockIdx.x * kD3W;
+  const int y0 = blockIdx.y * kD3H;
+  const int y = y0 - 1 + t.w;
+  t.xl = t.x0 + 4 * t.lane;
+  t.c = 4 * t.lane + 4;
+  t.X = static_cast<int>(g.X);
+  t.Z = static_cast<int>(g.Z);
+  t.XY = g.XY;
+  t.rowbase = static_cast<int64_t>(y) * t.X;
+  t.row_in = y >= 0 && y < static_cast<int>(g.Y);
+  t.cells = t.w <= kD3H;
+  t.out = t.w >= 1 && t.w <= kD3H && t.row_in;
+  const int s0 = blockIdx.z * chunk;
+  t.s1 = min(s0 + chunk, t.Z);
+  D3State A, B;
+  float4 pa, pb;  // values of planes p+1 (pa) and p+2 (pb) at an even step
+  float ha, hb;
+  {
+    float4 v;
+    float h;
+    d3_load<kVec>(t, s0 - 1, v, h);
+    d3_keys(t, s0 - 1, v, h, A.k, A.kh);
+    d3_publish(t, S.skey[0], A.k, A.kh);
+    d3_load<kVec>(t, s0, pa, ha);
+    d3_load<kVec>(t, s0 + 1, pb, hb);
+  }
+  __syncthreads();
+  // planes p = s0-1 .. s1 (the last step may run one past s1; it writes nothing)
+  for (int p = s0 - 1; p <= t.s1; p += 2) {
+    d3_step<0, kVec>(t, S, p, s0, A, B, pa, ha);
+    __syncthreads();
+    d3_step<1, kVec>(t, S, p + 1, s0, B, A, pb, hb);
+    __syncthreads();
+  }
+}
+
 // K1b (k_detect_kind, the full detect sweep) is defined with the subloop helpers below.
 
 // Counts of the first-match classes (detect_false_critical, edit_engine.cpp:134-158)

@@ -60,7 +60,10 @@ def test_directions_labels_golden(P, golden):
 
 
 @pytest.mark.parametrize("dims,dt", [([512, 512], np.float32), ([177, 95, 48], np.float32),
-                                     ([64, 33, 17], np.float64), ([3600, 240], np.float32)])
+                                     ([64, 33, 17], np.float64), ([3600, 240], np.float32),
+                                     ([256, 64, 40], np.float32), ([260, 30, 21], np.float32),
+                                     ([131, 17, 9], np.float32), ([4, 3, 2], np.float32),
+                                     ([2, 2, 2], np.float32)])
 def test_directions_labels_vs_oracle(P, oracle_lib, dims, dt):
     from paper_2406_09423_b200 import inputs as I
     rng = np.random.default_rng(7)
