@@ -1165,7 +1165,8 @@ struct TileStore {
 };
 
 // Phase 1.  Writes the provisional label (root, or first vertex outside the
-// tile) to prov and fin, and the tile's distinct exits to the tile store.
+// tile) to prov, fin[r] = r at roots, and the tile's distinct exits to the
+// tile store.
 // tile_list == nullptr: CTA i handles tile i.
 template <int DIM>
 __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
@@ -1285,7 +1286,9 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
                   tlz = t >> (TL::LX + TL::LY);
         const uint32_t res = base + tlx + g.X * tly + g.XY * tlz + soff[c];  // soff[15] = 0
         (fam ? m : M)[gi] = res;
-        (fam ? finm : finM)[gi] = res;
+        // fin is only ever read at provisional-label values: roots (here) and
+        // exits (seeded by k_exit_reset), so non-roots need no fin write
+        if (res == gi) (fam ? finm : finM)[gi] = res;
         if (t == i && c != kSelf) {
           const int hx = tlx + sd[0][c] + 1, hy = tly + sd[1][c] + 1;
           const int hz = DIM == 2 ? 0 : tlz + sd[2][c] + 1;
