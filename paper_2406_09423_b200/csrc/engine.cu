@@ -150,6 +150,7 @@ struct Workspace {
   DevBuf tE, tEcnt, toldfin, tdirty, taffected, tbits, tcnt, tlist;  // label-tile store
   DevBuf xbuf;  // sparse R pass: crossing lists X (2 families x 2 buffers)
   DevBuf cbits; // 1 bit per 64-vertex chunk whose direction codes changed
+  DevBuf cstamp; // per 64-vertex chunk: mark of the last batch that changed a code (k_detect_dirty)
   Ctl* ctl = nullptr;
   Ctl* hctl = nullptr;  // pinned mirror
   uint32_t next_batch = 1, next_mark = 1;
@@ -199,7 +200,7 @@ struct Workspace {
   }
   void release() {
     for (DevBuf* b : {&f, &g, &fdir, &gdir, &touched, &stamp, &fmark, &lab, &fin, &lists, &tiles,
-                      &tE, &tEcnt, &toldfin, &tdirty, &taffected, &tbits, &tcnt, &tlist, &xbuf, &cbits})
+                      &tE, &tEcnt, &toldfin, &tdirty, &taffected, &tbits, &tcnt, &tlist, &xbuf, &cbits, &cstamp})
       b->release();
     next_batch = next_mark = 1;
   }
@@ -217,11 +218,13 @@ struct Workspace {
     lab.ensure(np * 16);    // fM fm gM gm (u32)
     fin.ensure(np * 8);     // exit finals (finM finm), see k_exit_*
     cbits.ensure((n + 2047) / 2048 * 4 + 4);
+    fresh |= cstamp.ensure((n + 63) / 64 * 4 + 4);
     lists.ensure(np * 16);  // list0 list1 S F (u32); reused as the u64+T EditSet
     tiles.ensure(((n + kCompactTile - 1) / kCompactTile + 1) * 4);
     if (fresh || next_batch > 0xF0000000u || next_mark > 0xF0000000u) {
       CK(cudaMemsetAsync(stamp.p, 0, stamp.cap, stream));
       CK(cudaMemsetAsync(fmark.p, 0, fmark.cap, stream));
+      CK(cudaMemsetAsync(cstamp.p, 0, cstamp.cap, stream));
       next_batch = next_mark = 1;
     }
   }
@@ -272,6 +275,8 @@ Workspace& workspace(int device) {
 constexpr uint32_t kSmallBatchMax = 4096;
 // worklists above n / kHugeBatchDivisor are run by host-launched streaming kernels
 uint32_t kHugeBatchDivisor = 64;  // tunable via MSSZ_HUGE_DIVISOR (experiments)
+// R batches applying more than n / kRHugeDivisor edits refresh with a full sweep
+uint32_t kRHugeDivisor = 512;     // tunable via MSSZ_RHUGE_DIVISOR
 // R iterations after one with fewer than n / kSparseMismDivisor mismatches use the
 // sparse pass; it gives up when Up(X) exceeds n / kSparseUpDivisor vertices
 uint32_t kSparseMismDivisor = 1024;
@@ -316,6 +321,11 @@ struct Engine {
   uint32_t x_n[2] = {0, 0};
   size_t prof_n = 0;
   std::vector<int> prof_cls;
+  // incremental subloop detection: kind k's list was empty at mark end_mark[k]
+  // and every g-code change since then stamped its chunk (k_detect_dirty);
+  // a full direction sweep invalidates that (fresh[k] = false)
+  uint32_t end_mark[4] = {0, 0, 0, 0};
+  bool fresh[4] = {false, false, false, false};
   float dir_ms = 0.f, lab_ms = 0.f;
 
   Engine(Workspace& w, const Geom& g, const mssz_cu_options& o) : ws(w), geo(g), opt(o) {}
@@ -346,8 +356,10 @@ struct Engine {
     s.ctl = ws.ctl;
     s.tdirty = nullptr;
     s.cdirty = ws.cbits.as<uint32_t>();
+    s.cstamp = ws.cstamp.as<uint32_t>();
     s.own_lo = s.act_lo = 0;
     s.own_n = s.act_n = geo.n;
+    s.tune = std::getenv("MSSZ_TUNE") ? static_cast<uint32_t>(std::atoi(std::getenv("MSSZ_TUNE"))) : 0u;
   }
 
   // Per-kernel-class device time (CUDA events on the launching stream), only
@@ -383,6 +395,8 @@ struct Engine {
   void directions(const T* vals, uint8_t* dir) {
     if (dir == s.gdir && s.cdirty)  // every code may change: X must re-evaluate all chunks
       CK(cudaMemsetAsync(s.cdirty, 0xFF, (n() + 2047) / 2048 * 4, ws.stream));
+    if (dir == s.gdir)
+      for (bool& f : fresh) f = false;
     pre(kProfDirections);
     const uint64_t want = static_cast<uint64_t>(ws.sms) * 8;
     if (geo.ndims == 2) {
@@ -610,6 +624,7 @@ struct Engine {
   int coop_grid() {
     if (coop_blocks) return coop_blocks;
     if (const char* h = std::getenv("MSSZ_HUGE_DIVISOR")) kHugeBatchDivisor = std::max(1, std::atoi(h));
+    if (const char* h = std::getenv("MSSZ_RHUGE_DIVISOR")) kRHugeDivisor = std::max(1, std::atoi(h));
     if (const char* h = std::getenv("MSSZ_SPARSE_DIVISOR")) kSparseMismDivisor = std::max(1, std::atoi(h));
     int occ = 0;
     if (geo.ndims == 2)
@@ -687,8 +702,12 @@ struct Engine {
     reset_ctl();
     ws.push_ctl();
     pre(kProfDetectKind);
-    k_detect_kind<<<grid_for((n() + 15) / 16, 256, ws.sms, 16), 256, 0, ws.stream>>>(
-        s.fdir, s.gdir, n(), kind, s.list[cur], &ws.ctl->list_count[cur]);
+    if (fresh[kind])
+      k_detect_dirty<<<grid_for((n() + 15) / 16, 256, ws.sms, 16), 256, 0, ws.stream>>>(
+          s.fdir, s.gdir, n(), s.cstamp, end_mark[kind], kind, s.list[cur], &ws.ctl->list_count[cur]);
+    else
+      k_detect_kind<<<grid_for((n() + 15) / 16, 256, ws.sms, 16), 256, 0, ws.stream>>>(
+          s.fdir, s.gdir, n(), kind, s.list[cur], &ws.ctl->list_count[cur]);
     launched(kProfDetectKind);
     ++st.detect_sweeps;
     const uint32_t batch_base = ws.next_batch, mark_base = ws.next_mark;
@@ -756,7 +775,11 @@ struct Engine {
     for (;;) {
       ++st.c_passes;
       uint64_t pass_edits = 0;
-      for (int kind = 0; kind < 4; ++kind) pass_edits += run_subloop(kind);
+      for (int kind = 0; kind < 4; ++kind) {
+        pass_edits += run_subloop(kind);
+        end_mark[kind] = ws.next_mark;  // every later batch uses marks >= this
+        fresh[kind] = true;
+      }
       if (pass_edits) r_full_valid = false;  // the tile store no longer matches gdir
       if (pass_edits == 0) return;
     }
@@ -965,7 +988,7 @@ struct Engine {
       if (applied == 0)
         fail(MSSZ_CU_ERR_NON_CONVERGENCE, "R-loop stalled: every troublemaker is at its floor");
       const uint32_t mark = ws.next_mark++;
-      if (applied > n() / kHugeBatchDivisor) {
+      if (applied > n() / kRHugeDivisor) {
         directions(s.g, s.gdir);  // large batch: one streaming sweep beats 15 RMWs per edit
         CK(cudaMemsetAsync(ts.dirty, 1, ts.ntiles, ws.stream));
         last_frontier = false;

@@ -643,6 +643,8 @@ struct State {
   // frontier refreshes only vertices in [act_lo, act_lo + act_n) (owned planes plus
   // one halo plane per side).  Single device: both ranges are the whole grid.
   uint32_t own_lo, own_n, act_lo, act_n;
+  uint32_t tune;  // experiment bits (MSSZ_TUNE): 1 = frontier claims without the pre-check load
+  uint32_t* cstamp;  // per 64-vertex chunk: mark id of the last batch that changed a code in it
 };
 
 // claim (edit_engine.cpp:160-169) + lower_step (:75-86): the first claimant of
@@ -733,14 +735,24 @@ __device__ __forceinline__ void slot_delta(int k, int& dx, int& dy, int& dz) {
   }
 }
 
-// Re-evaluates gdir on S ∪ N(S) (the only vertices whose direction can change
-// after a batch), each vertex once (fmark dedupe), and collects them in F.
-// One lane per (edited vertex, candidate slot): 16 lanes per vertex in 3D
-// (self + 14 slots), 8 in 2D, so every lane has one claim and one direction
-// evaluation in flight instead of a serial chain of 15.
-// next (optional, C-loop): instead of collecting F, append every frontier
+// Re-evaluates gdir where a batch can have changed it, each vertex once (fmark
+// dedupe), and collects the re-evaluated vertices in F.
+// One lane per (edited vertex t, u in {t} ∪ N(t)): 16 lanes per edit in 3D,
+// 8 in 2D.  A batch only LOWERS values, so for u (with all lowered values
+// final):
+//   * asc(u) = SoS-argmax over {u} ∪ N(u) can change only if asc(u) itself
+//     was lowered (any other member only decreased);
+//   * desc(u) can change only if some lowered t in {u} ∪ N(u) now beats the
+//     current minimum desc(u) in SoS order.
+// So lane (t, u) recomputes u only when asc(u) == t or t <_SoS desc(u): two
+// loads decide, and every vertex whose code can change is recomputed by the
+// lane of the edit that changed it.  Unchanged codes keep their class, so the
+// old worklist's entries that were not recomputed stay valid (rebuild_retry).
+// A stale gdir[u] read (another lane recomputing u concurrently) is harmless:
+// the recompute reads final values, and a claim lost to it changes nothing.
+// next (optional, C-loop): instead of collecting F, append every re-evaluated
 // vertex that is of `kind` under its refreshed code straight to the next
-// worklist (f_count then only counts the frontier).
+// worklist (f_count then only counts them).
 template <class T, int DIM>
 __device__ __forceinline__ void frontier_update(const State<T>& s, uint32_t ns, uint32_t mark,
                                                 uint32_t* f_count, uint64_t tid, uint64_t stride,
@@ -767,13 +779,22 @@ __device__ __forceinline__ void frontier_update(const State<T>& s, uint32_t ns, 
         const uint32_t ux = x + dx, uy = y + dy, uz = z + dz;
         if (ux < s.geo.X && uy < s.geo.Y && (DIM == 2 || uz < s.geo.Z) &&
             (u = ux + s.geo.X * uy + s.geo.XY * uz) - s.act_lo < s.act_n) {
-          if (__ldcg(s.fmark + u) != mark && atomicExch(&s.fmark[u], mark) != mark) {
+          const uint32_t cu = __ldcg(s.gdir + u);
+          const uint32_t ca = cu & 15u, cd = cu >> 4;
+          const uint32_t um = cd == kSelf ? u : u + s.geo.off[cd];
+          bool fire = (ca == kSelf ? u : u + s.geo.off[ca]) == sv;
+          if (!fire && um != sv) {
+            const auto kt = okey(__ldcg(s.g + sv)), km = okey(__ldcg(s.g + um));
+            fire = kt < km || (kt == km && sv < um);
+          }
+          if (fire && __ldcg(s.fmark + u) != mark && atomicExch(&s.fmark[u], mark) != mark) {
             mine = true;
             const uint8_t code =
                 static_cast<uint8_t>(direction_code<T, DIM, true>(s.g, s.geo, u, ux, uy, uz));
             if (next) keep = kind_match(kind, __ldg(s.fdir + u), code);
             if (s.gdir[u] != code) {
               s.gdir[u] = code;
+              if (s.cstamp && s.cstamp[u >> 6] != mark) s.cstamp[u >> 6] = mark;
               if (s.tdirty) s.tdirty[label_tile_of<DIM>(s.geo, ux, uy, uz)] = 1;
               if (s.cdirty) {  // test first: neighbouring edits share the chunk bit
                 const uint32_t bit = 1u << ((u >> 6) & 31);
@@ -799,10 +820,10 @@ __device__ __forceinline__ void frontier_update(const State<T>& s, uint32_t ns, 
   }
 }
 
-// New worklist = (old list minus frontier) ∪ {u in frontier : kind(u)}.  The
-// second part is appended by frontier_update; here only the retry items
-// (the old-list entries that can lie outside the frontier) are checked.
-// Exact: only frontier vertices can change class after a batch.
+// New worklist = (old list minus re-evaluated) ∪ {u re-evaluated : kind(u)}.
+// The second part is appended by frontier_update; here the old entries that
+// were not re-evaluated are kept.  Exact: a vertex whose code did not change
+// keeps its class.
 __device__ __forceinline__ void rebuild_retry(const uint32_t* __restrict__ retry, uint32_t nr,
                                               const uint32_t* __restrict__ fmark, uint32_t mark,
                                               uint32_t* nxt, uint32_t* nxt_count, uint64_t tid,
@@ -890,6 +911,44 @@ __global__ void __launch_bounds__(256) k_detect_kind(const uint8_t* __restrict__
                        static_cast<uint64_t>(gridDim.x) * blockDim.x);
 }
 
+// detect_kind restricted to the 64-vertex chunks whose codes changed since
+// mark `since` (cstamp[c] >= since).  At the end of a subloop its kind's list
+// is empty, and a vertex can only change class when its g-direction changes,
+// so at the kind's next subloop these chunks hold every item.
+__global__ void __launch_bounds__(256) k_detect_dirty(const uint8_t* __restrict__ fdir,
+                                                      const uint8_t* __restrict__ gdir, uint32_t n,
+                                                      const uint32_t* __restrict__ cstamp, uint32_t since,
+                                                      int kind, uint32_t* __restrict__ list,
+                                                      uint32_t* count) {
+  const uint64_t nq = (static_cast<uint64_t>(n) + 15) / 16;  // 16-vertex groups, 4 per chunk
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t wb = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) & ~uint64_t(31); wb < nq;
+       wb += stride) {
+    const uint64_t q = wb + (threadIdx.x & 31);
+    uint32_t mask = 0;
+    if (q < nq && __ldg(cstamp + (q >> 2)) >= since) {
+      const uint64_t v0 = q * 16;
+      if (v0 + 16 <= n) {
+        const uint4 f = __ldg(reinterpret_cast<const uint4*>(fdir + v0));
+        const uint4 g = __ldg(reinterpret_cast<const uint4*>(gdir + v0));
+        mask = bytes_to_nibble(kind_bytes(kind, f.x, g.x)) | bytes_to_nibble(kind_bytes(kind, f.y, g.y)) << 4 |
+               bytes_to_nibble(kind_bytes(kind, f.z, g.z)) << 8 | bytes_to_nibble(kind_bytes(kind, f.w, g.w)) << 12;
+      } else {
+        for (int j = 0; j < 16; ++j)
+          if (v0 + j < n && kind_match(kind, fdir[v0 + j], gdir[v0 + j])) mask |= 1u << j;
+      }
+    }
+    if (!__any_sync(0xffffffffu, mask != 0)) continue;
+    const uint32_t base = warp_reserve(__popc(mask), count);
+    uint32_t pos = base;
+    while (mask) {
+      const int j = __ffs(mask) - 1;
+      mask &= mask - 1;
+      list[pos++] = static_cast<uint32_t>(q * 16 + j);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Persistent subloop (run_subloop, edit_engine.cpp:246-278): detect → fix →
 // refresh until the kind's list is empty, entirely on the device, in one
@@ -922,14 +981,14 @@ __device__ BatchResult big_batch(const State<T>& s, cg::grid_group& grid, int ki
   const uint32_t batch = batch_base + 2 * it, mark = mark_base + it;
   uint64_t t0 = 0, t1 = 0, t2 = 0;
   if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  fix_batch(s, s.list[cur], n, rule, batch, &ctl->s_count, tid, stride, s.F, &ctl->retry_count);
+  fix_batch(s, s.list[cur], n, rule, batch, &ctl->s_count, tid, stride);
   grid.sync();
   uint32_t applied = *reinterpret_cast<volatile uint32_t*>(&ctl->s_count);
   if (applied == 0 && kind == 1) {
     grid.sync();  // every thread has read applied == 0 before the fallback appends to S
     if (tid == 0) ctl->retry_count = 0;
     grid.sync();
-    fix_batch(s, s.list[cur], n, 2, batch + 1, &ctl->s_count, tid, stride, s.F, &ctl->retry_count);
+    fix_batch(s, s.list[cur], n, 2, batch + 1, &ctl->s_count, tid, stride);
     grid.sync();
     applied = *reinterpret_cast<volatile uint32_t*>(&ctl->s_count);
   }
@@ -946,8 +1005,7 @@ __device__ BatchResult big_batch(const State<T>& s, cg::grid_group& grid, int ki
   grid.sync();
   if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
   const uint32_t nf = *reinterpret_cast<volatile uint32_t*>(&ctl->f_count);
-  const uint32_t nr = *reinterpret_cast<volatile uint32_t*>(&ctl->retry_count);
-  rebuild_retry(s.F, nr, s.fmark, mark, s.list[cur ^ 1], &ctl->list_count[cur ^ 1], tid, stride);
+  rebuild_retry(s.list[cur], n, s.fmark, mark, s.list[cur ^ 1], &ctl->list_count[cur ^ 1], tid, stride);
   grid.sync();
   if (tid == 0) {
     uint64_t t3;
@@ -970,14 +1028,14 @@ __device__ BatchResult small_batch(const State<T>& s, int kind, uint32_t n, uint
   const uint64_t tid = threadIdx.x, stride = blockDim.x;
   const int rule = (kind == 0 || kind == 3) ? 0 : 1;
   const uint32_t batch = batch_base + 2 * it, mark = mark_base + it;
-  fix_batch(s, s.list[cur], n, rule, batch, &cnt[0], tid, stride, s.F, &cnt[3]);
+  fix_batch(s, s.list[cur], n, rule, batch, &cnt[0], tid, stride);
   __syncthreads();
   uint32_t applied = *reinterpret_cast<volatile uint32_t*>(&cnt[0]);
   if (applied == 0 && kind == 1) {
     __syncthreads();
     if (threadIdx.x == 0) cnt[3] = 0;
     __syncthreads();
-    fix_batch(s, s.list[cur], n, 2, batch + 1, &cnt[0], tid, stride, s.F, &cnt[3]);
+    fix_batch(s, s.list[cur], n, 2, batch + 1, &cnt[0], tid, stride);
     __syncthreads();
     applied = *reinterpret_cast<volatile uint32_t*>(&cnt[0]);
   }
@@ -985,8 +1043,7 @@ __device__ BatchResult small_batch(const State<T>& s, int kind, uint32_t n, uint
   frontier_update<T, DIM>(s, applied, mark, &cnt[1], tid, stride, kind, s.list[cur ^ 1], &cnt[2]);
   __syncthreads();
   const uint32_t nf = *reinterpret_cast<volatile uint32_t*>(&cnt[1]);
-  const uint32_t nr = *reinterpret_cast<volatile uint32_t*>(&cnt[3]);
-  rebuild_retry(s.F, nr, s.fmark, mark, s.list[cur ^ 1], &cnt[2], tid, stride);
+  rebuild_retry(s.list[cur], n, s.fmark, mark, s.list[cur ^ 1], &cnt[2], tid, stride);
   __syncthreads();
   if (threadIdx.x == 0) {
     s.ctl->list_count[cur ^ 1] = cnt[2];

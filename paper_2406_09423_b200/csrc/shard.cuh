@@ -780,7 +780,7 @@ struct SlabEngine {
       const uint32_t batch = batch_base + 2 * it, mark = mark_base + it;
       // the fix runs before the global emptiness test: when every list is
       // empty it is a no-op, and the test then costs no extra round trip
-      fix(rule, batch, S.list[cur], &ws.ctl->list_count[cur], true);
+      fix(rule, batch, S.list[cur], &ws.ctl->list_count[cur], false);
       gather();
       const uint64_t total = sum([](const Rec& r) { return r.list; });
       if (total == 0) break;
@@ -789,7 +789,7 @@ struct SlabEngine {
         fail(MSSZ_CU_ERR_NON_CONVERGENCE, "%s subloop exceeded its iteration cap", kKindName[kind]);
       uint64_t applied = sum([](const Rec& r) { return r.applied; });
       if (applied == 0 && kind == 1) {  // FPmin fallback (edit_engine.cpp:262-268)
-        fix(2, batch + 1, S.list[cur], &ws.ctl->list_count[cur], true);
+        fix(2, batch + 1, S.list[cur], &ws.ctl->list_count[cur], false);
         gather();
         applied = sum([](const Rec& r) { return r.applied; });
       }
@@ -810,7 +810,7 @@ struct SlabEngine {
         eng.launched(kProfFrontier);
         eng.pre(kProfFrontier);
         k_slab_rebuild<<<blocks(sb.hrec[pl.r].list, 8), 256, 0, ws.stream>>>(
-            S.F, &ws.ctl->retry_count, S.fmark, mark, S.list[cur ^ 1], &ws.ctl->list_count[cur ^ 1]);
+            S.list[cur], &ws.ctl->list_count[cur], S.fmark, mark, S.list[cur ^ 1], &ws.ctl->list_count[cur ^ 1]);
         eng.launched(kProfFrontier);
       }
       st().frontier_vertices += ns;  // refresh seeds (own targets + received halo targets)
@@ -895,7 +895,7 @@ struct SlabEngine {
       const uint32_t ns = static_cast<uint32_t>(sb.hrec[pl.r].applied) + nrecv;
       const uint32_t mark = ws.next_mark++;
       CK(cudaMemsetAsync(&ws.ctl->f_count, 0, sizeof(uint32_t), ws.stream));
-      if (applied > n_glob / kHugeBatchDivisor) {
+      if (applied > n_glob / kRHugeDivisor) {
         eng.directions(s().g, s().gdir);
         last_frontier = false;
       } else {
