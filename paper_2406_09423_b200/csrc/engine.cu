@@ -279,7 +279,7 @@ uint32_t kHugeBatchDivisor = 64;  // tunable via MSSZ_HUGE_DIVISOR (experiments)
 uint32_t kRHugeDivisor = 512;     // tunable via MSSZ_RHUGE_DIVISOR
 // R iterations after one with fewer than n / kSparseMismDivisor mismatches use the
 // sparse pass; it gives up when Up(X) exceeds n / kSparseUpDivisor vertices
-uint32_t kSparseMismDivisor = 1024;
+uint32_t kSparseMismDivisor = 64;
 uint32_t kSparseUpDivisor = 16;
 uint32_t kSparseMaxLevels = 256;  // deeper upstream trees go to the full pass
 
