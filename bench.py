@@ -362,6 +362,32 @@ def main():
                     "mean_launch_us": per_launch_ms * 1e3,
                     "share_of_device_time": graded[top]["ms"] / total_ms if total_ms else None}
 
+    # ---- verification report of the corrected field, device-resident
+    verify = None
+    if not sharded:
+        g = dfh.clone()
+        g[d_idx[:count]] = d_val[:count]
+        torch.cuda.synchronize()
+        vopts = P.DeriveOptions(device=dist.local)
+        P.build_report_device(topo, df.data_ptr(), g.data_ptr(), xi, dtype, count, 0, vopts,
+                              stream.cuda_stream)  # warm
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        flush.fill_(1.0)
+        a.record(stream)
+        rep = P.build_report_device(topo, df.data_ptr(), g.data_ptr(), xi, dtype, count, 0, vopts,
+                                    stream.cuda_stream)
+        b.record(stream)
+        b.synchronize()
+        del g
+        vms = a.elapsed_time(b)
+        verify = {"ms": vms, "value": n / (vms * 1e-3) / 1e6, "unit": UNIT,
+                  "api": "mssz_cu_verify_device (build_report, tools/mssz.cpp:84-104)",
+                  "passed": rep.passed(), "mss_distortion": rep.mss_distortion, "psnr": rep.psnr,
+                  "bound_violations": rep.bound_violations, "edit_ratio": rep.edit_ratio,
+                  "false_extrema": [rep.fp_max, rep.fp_min, rep.fn_max, rep.fn_min],
+                  "gpu_launches": rep.kernel_launches}
+
     # ---- e2e through the host API with pinned buffers
     e2e = None
     if not args.no_e2e:
@@ -431,6 +457,7 @@ def main():
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "verify": verify,
         "gpu_launches": int(dist.sum(float(sum(s.kernel_launches for s in stats)))),
         "clocks": clk,
         "edit_stats": {"outer_iterations": st.outer_iterations, "c_passes": st.c_passes,

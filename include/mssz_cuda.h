@@ -223,6 +223,38 @@ int mssz_cu_comm_destroy(mssz_cu_comm* comm);
 MSSZ_CU_DECLARE_SLAB(f32, float)
 MSSZ_CU_DECLARE_SLAB(f64, double)
 
+/* ---- verification report: build_report, tools/mssz.cpp:84-104 ----
+ * VerificationReport (metrics.hpp:14-23) field for field, then B200 extras.  The
+ * reference CLI's `verify` exits 0 iff mss_distortion == 0 && bound_violations == 0
+ * (tools/mssz.cpp:250).  psnr's sum of squares is a deterministic tree reduction
+ * (reference: sequential), equal to 1e-12 relative; every count is exact. */
+typedef struct mssz_cu_report {
+  double mss_distortion;      /* label mismatches / N (metrics.cpp:12-15) */
+  double right_labeled_ratio; /* 1 - mss_distortion */
+  double psnr;                /* dB, +inf when rmse == 0 (metrics.cpp:18-32) */
+  double edit_ratio;          /* edit_count / N */
+  double ocr;                 /* original bytes / archive bytes (0 when archive_bytes == 0) */
+  double obr;                 /* 8 * archive bytes / N */
+  uint64_t bound_violations;  /* |f - g| > xi in double (metrics.cpp:46-56) */
+  uint64_t fp_max, fp_min, fn_max, fn_min; /* first-match classes (tools/mssz.cpp:69-82) */
+  /* B200 extras */
+  uint64_t mismatches;
+  double sum_sq, value_lo, value_hi;
+  double device_seconds;
+  uint64_t kernel_launches;
+} mssz_cu_report;
+
+#define MSSZ_CU_DECLARE_VERIFY(SUF, T)                                                              \
+  int mssz_cu_verify_##SUF(int ndims, const uint64_t* dims, const T* original, const T* candidate,  \
+                           double xi, uint64_t edit_count, uint64_t archive_bytes,                   \
+                           const mssz_cu_options* opt, mssz_cu_report* out);                         \
+  int mssz_cu_verify_device_##SUF(int ndims, const uint64_t* dims, const T* d_original,             \
+                                  const T* d_candidate, double xi, uint64_t edit_count,              \
+                                  uint64_t archive_bytes, const mssz_cu_options* opt,                \
+                                  mssz_cu_report* out, void* cuda_stream);
+MSSZ_CU_DECLARE_VERIFY(f32, float)
+MSSZ_CU_DECLARE_VERIFY(f64, double)
+
 #ifdef __cplusplus
 }
 #endif

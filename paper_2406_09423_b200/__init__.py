@@ -33,6 +33,7 @@ __all__ = [
     "compute_direction_codes", "compute_labels", "classify_critical", "detect_false_critical",
     "detect_kind", "lower_step", "representable_floor", "apply_edits", "segmentation_equal",
     "library", "build", "slab_range", "derive_edits_slabs", "SlabComm",
+    "VerificationReport", "build_report", "build_report_device",
 ]
 
 FPMAX, FPMIN, FNMAX, FNMIN = 0, 1, 2, 3
@@ -277,7 +278,7 @@ EXPORTS = [
         "derive_edits", "derive_edits_into", "derive_edits_device", "compute_directions",
         "compute_direction_codes", "detect_false_critical", "detect_kind", "lower_step",
         "representable_floor", "apply_edits", "derive_edits_slab", "derive_edits_slab_device",
-        "derive_edits_slabs_local")
+        "derive_edits_slabs_local", "verify", "verify_device")
 ]
 
 _lib = None
@@ -655,3 +656,73 @@ class SlabComm:
             C.byref(count), C.byref(offset), C.byref(st), C.c_void_p(stream or None))
         _check(rc)
         return count.value, offset.value, st.fill(EditStats())
+
+
+# ---------------------------------------------------------------- verification report
+@dataclass
+class VerificationReport:
+    """VerificationReport (metrics.hpp:14-23) plus the device extras."""
+
+    mss_distortion: float = 0.0
+    right_labeled_ratio: float = 1.0
+    psnr: float = 0.0
+    edit_ratio: float = 0.0
+    ocr: float = 0.0
+    obr: float = 0.0
+    bound_violations: int = 0
+    fp_max: int = 0
+    fp_min: int = 0
+    fn_max: int = 0
+    fn_min: int = 0
+    mismatches: int = 0
+    sum_sq: float = 0.0
+    value_lo: float = 0.0
+    value_hi: float = 0.0
+    device_seconds: float = 0.0
+    kernel_launches: int = 0
+
+    def passed(self) -> bool:
+        """The reference CLI's verify exit criterion (tools/mssz.cpp:250)."""
+        return self.mss_distortion == 0.0 and self.bound_violations == 0
+
+
+class _Report(C.Structure):
+    _fields_ = [
+        ("mss_distortion", C.c_double), ("right_labeled_ratio", C.c_double), ("psnr", C.c_double),
+        ("edit_ratio", C.c_double), ("ocr", C.c_double), ("obr", C.c_double),
+        ("bound_violations", C.c_uint64), ("fp_max", C.c_uint64), ("fp_min", C.c_uint64),
+        ("fn_max", C.c_uint64), ("fn_min", C.c_uint64), ("mismatches", C.c_uint64),
+        ("sum_sq", C.c_double), ("value_lo", C.c_double), ("value_hi", C.c_double),
+        ("device_seconds", C.c_double), ("kernel_launches", C.c_uint64),
+    ]
+
+    def to_report(self) -> VerificationReport:
+        return VerificationReport(**{name: getattr(self, name) for name, _ in self._fields_})
+
+
+def build_report(topo: GridTopology, original, candidate, xi: float, edit_count: int = 0,
+                 archive_bytes: int = 0, opts: Optional[DeriveOptions] = None) -> VerificationReport:
+    """build_report<T> (tools/mssz.cpp:84-104) on the GPU; host arrays in."""
+    f = _field(topo, original, "original")
+    g = _field(topo, candidate, "candidate", f.dtype)
+    keep: list = []
+    co = _options(opts, f.dtype, keep)
+    r = _Report()
+    _check(getattr(library(), f"mssz_cu_verify_{_suf(f.dtype)}")(
+        topo.ndims, _dims(topo), _p(f), _p(g), C.c_double(xi), C.c_uint64(edit_count),
+        C.c_uint64(archive_bytes), C.byref(co), C.byref(r)))
+    return r.to_report()
+
+
+def build_report_device(topo: GridTopology, d_f: int, d_g: int, xi: float, dtype=np.float32,
+                        edit_count: int = 0, archive_bytes: int = 0,
+                        opts: Optional[DeriveOptions] = None, stream: int = 0) -> VerificationReport:
+    """Device-resident variant (CUDA pointers, optional stream)."""
+    keep: list = []
+    co = _options(opts, dtype, keep)
+    r = _Report()
+    _check(getattr(library(), f"mssz_cu_verify_device_{_suf(dtype)}")(
+        topo.ndims, _dims(topo), C.c_void_p(d_f), C.c_void_p(d_g), C.c_double(xi),
+        C.c_uint64(edit_count), C.c_uint64(archive_bytes), C.byref(co), C.byref(r),
+        C.c_void_p(stream or None)))
+    return r.to_report()

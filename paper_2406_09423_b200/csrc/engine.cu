@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
+#include <limits>
 #include <chrono>
 #include <cstdarg>
 #include <cstdio>
@@ -1581,3 +1583,4 @@ int mssz_cu_classify_critical(uint64_t n, const uint64_t* asc, const uint64_t* d
 }  // extern "C"
 
 #include "shard_api.cuh"
+#include "verify.cuh"
