@@ -255,6 +255,14 @@ typedef struct mssz_cu_report {
 MSSZ_CU_DECLARE_VERIFY(f32, float)
 MSSZ_CU_DECLARE_VERIFY(f64, double)
 
+/* The `mss` subcommand (tools/mssz.cpp:260-266): SegmentationLabels of a field,
+ * compute_labels(compute_directions(values)) in one device pass; u64 max and min
+ * labels (mss.hpp:37-42).  export_labels (mss.cpp:135-145) writes M then m as u64 LE. */
+int mssz_cu_segmentation_f32(int ndims, const uint64_t* dims, const float* values, uint64_t* max_label,
+                             uint64_t* min_label);
+int mssz_cu_segmentation_f64(int ndims, const uint64_t* dims, const double* values, uint64_t* max_label,
+                             uint64_t* min_label);
+
 #ifdef __cplusplus
 }
 #endif

@@ -33,7 +33,7 @@ __all__ = [
     "compute_direction_codes", "compute_labels", "classify_critical", "detect_false_critical",
     "detect_kind", "lower_step", "representable_floor", "apply_edits", "segmentation_equal",
     "library", "build", "slab_range", "derive_edits_slabs", "SlabComm",
-    "VerificationReport", "build_report", "build_report_device",
+    "VerificationReport", "build_report", "build_report_device", "segmentation", "export_labels",
 ]
 
 FPMAX, FPMIN, FNMAX, FNMIN = 0, 1, 2, 3
@@ -278,7 +278,7 @@ EXPORTS = [
         "derive_edits", "derive_edits_into", "derive_edits_device", "compute_directions",
         "compute_direction_codes", "detect_false_critical", "detect_kind", "lower_step",
         "representable_floor", "apply_edits", "derive_edits_slab", "derive_edits_slab_device",
-        "derive_edits_slabs_local", "verify", "verify_device")
+        "derive_edits_slabs_local", "verify", "verify_device", "segmentation")
 ]
 
 _lib = None
@@ -726,3 +726,20 @@ def build_report_device(topo: GridTopology, d_f: int, d_g: int, xi: float, dtype
         C.c_uint64(edit_count), C.c_uint64(archive_bytes), C.byref(co), C.byref(r),
         C.c_void_p(stream or None)))
     return r.to_report()
+
+
+def segmentation(topo: GridTopology, values) -> SegmentationLabels:
+    """compute_labels(compute_directions(values)) in one device pass (the `mss` subcommand)."""
+    v = _field(topo, values, "values")
+    M = np.empty(topo.vertex_count, np.uint64)
+    m = np.empty(topo.vertex_count, np.uint64)
+    _check(getattr(library(), f"mssz_cu_segmentation_{_suf(v.dtype)}")(
+        topo.ndims, _dims(topo), _p(v), _p(M), _p(m)))
+    return SegmentationLabels(M, m)
+
+
+def export_labels(labels: SegmentationLabels, path: str) -> None:
+    """export_labels (mss.cpp:135-145): the M array then the m array, u64 little-endian."""
+    with open(path, "wb") as fp:
+        fp.write(np.ascontiguousarray(labels.max_label, "<u8").tobytes())
+        fp.write(np.ascontiguousarray(labels.min_label, "<u8").tobytes())

@@ -160,10 +160,44 @@ void verify_entry(int ndims, const uint64_t* dims, const T* f, const T* g, doubl
   }
 }
 
+// The `mss` subcommand (tools/mssz.cpp:260-266): compute_labels(compute_directions(f))
+// in one device pass (K1 + tiled K3 with its finish phase), u64 labels out.
+template <class T>
+void segmentation_entry(int ndims, const uint64_t* dims, const T* values, uint64_t* M, uint64_t* m) {
+  const Geom geo = make_geom(ndims, dims);
+  if (!values || !M || !m) fail(MSSZ_CU_ERR_USAGE, "null pointer");
+  mssz_cu_options opt;
+  mssz_cu_default_options(&opt);
+  Workspace& ws = workspace(-1);
+  std::lock_guard<std::mutex> lk(ws.mu);
+  ws.ensure(geo.n, sizeof(T));
+  Engine<T> eng(ws, geo, opt);
+  eng.bind(ws.f.as<T>());
+  CK(cudaMemcpyAsync(ws.f.p, values, sizeof(T) * geo.n, cudaMemcpyHostToDevice, ws.stream));
+  eng.directions(ws.f.as<T>(), ws.fdir.as<uint8_t>());
+  eng.label_pass(ws.fdir.as<uint8_t>(), eng.lab(0), eng.lab(1), false, true);
+  const uint64_t np = (geo.n + 63) & ~uint64_t(63);
+  uint64_t* da = reinterpret_cast<uint64_t*>(ws.lists.p);
+  uint64_t* dd = da + np;
+  const uint32_t blocks = grid_for(geo.n, 256, ws.sms, 16);
+  k_u32_to_u64<<<blocks, 256, 0, ws.stream>>>(eng.lab(0), da, geo.n);
+  k_u32_to_u64<<<blocks, 256, 0, ws.stream>>>(eng.lab(1), dd, geo.n);
+  CK_LAUNCH();
+  CK(cudaMemcpyAsync(M, da, 8ull * geo.n, cudaMemcpyDeviceToHost, ws.stream));
+  CK(cudaMemcpyAsync(m, dd, 8ull * geo.n, cudaMemcpyDeviceToHost, ws.stream));
+  ws.sync();
+}
+
 }  // namespace
 }  // namespace mssz_b200
 
 extern "C" {
+int mssz_cu_segmentation_f32(int ndims, const uint64_t* dims, const float* values, uint64_t* M, uint64_t* m) {
+  return mssz_b200::guarded([&] { mssz_b200::segmentation_entry<float>(ndims, dims, values, M, m); });
+}
+int mssz_cu_segmentation_f64(int ndims, const uint64_t* dims, const double* values, uint64_t* M, uint64_t* m) {
+  return mssz_b200::guarded([&] { mssz_b200::segmentation_entry<double>(ndims, dims, values, M, m); });
+}
 #define MSSZ_CU_DEFINE_VERIFY(SUF, T)                                                                  \
   int mssz_cu_verify_##SUF(int ndims, const uint64_t* dims, const T* original, const T* candidate,     \
                            double xi, uint64_t edit_count, uint64_t archive_bytes,                      \

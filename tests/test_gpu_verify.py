@@ -115,3 +115,27 @@ def test_report_device_matches_host(P):
                                 stream=torch.cuda.current_stream().cuda_stream)
     for k in ("mismatches", "bound_violations", "fp_max", "fp_min", "fn_max", "fn_min", "sum_sq", "psnr"):
         assert getattr(dev, k) == getattr(host, k), k
+
+
+@pytest.mark.parametrize("dims,dt", [([177, 95, 48], np.float32), ([96, 64], np.float64),
+                                     ([128, 32, 16], np.float32)])
+def test_segmentation_matches_reference(P, golden, oracle_lib, dims, dt, tmp_path):
+    from paper_2406_09423_b200 import inputs as I
+    topo = P.build_topology(dims)
+    f = I.generate("random-smooth", dims, 4, dt)
+    lab = P.segmentation(topo, f)
+    a, b = oracle_lib.compute_directions(dims, f)
+    M, m = oracle_lib.compute_labels(dims, a, b)
+    assert np.array_equal(lab.max_label, M) and np.array_equal(lab.min_label, m)
+    out = tmp_path / "labels.bin"
+    P.export_labels(lab, str(out))
+    raw = np.frombuffer(out.read_bytes(), "<u8")
+    assert np.array_equal(raw[:f.size], M) and np.array_equal(raw[f.size:], m)
+    # the golden direction/label fields of the reference's own tests
+    meta, arr = golden
+    for case in meta["directions"]:
+        p = f"dir/{case['name']}/"
+        t = P.build_topology(case["dims"])
+        lab = P.segmentation(t, arr[p + "values"])
+        assert np.array_equal(lab.max_label, arr[p + "max_label"]), case["name"]
+        assert np.array_equal(lab.min_label, arr[p + "min_label"]), case["name"]
