@@ -1249,17 +1249,24 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
   for (int w = threadIdx.x; w < 2 * ((HBOX + 31) / 32); w += kLabelTileThreads)
     (&seen[0][0])[w] = 0u;
   if (threadIdx.x < 2) sexit_n[threadIdx.x] = 0;
-  __shared__ int8_t sd[3][16];
+  // per slot: global offset, local (in-tile) offset, faces of the tile it crosses
+  // (bit 0 -x, 1 +x, 2 -y, 3 +y, 4 -z, 5 +z); SELF = slot 15: offset 0, no face
   __shared__ int32_t soff[16];
+  __shared__ int32_t sloc[16];
+  __shared__ uint32_t sface[16];
+  __shared__ int32_t shalo[16];  // offset in the tile's halo box (exit dedupe bitmap)
+  constexpr int NROW = TL::TY * TL::TZ;  // tile rows (x runs)
+  __shared__ uint32_t rowbase[NROW];     // global id of each row's first vertex
   if (threadIdx.x < 16) {
     int dx = 0, dy = 0, dz = 0;
 #pragma unroll
     for (int k = 0; k < NS; ++k)
       if (k == static_cast<int>(threadIdx.x)) stencil<DIM>(k, dx, dy, dz);
-    sd[0][threadIdx.x] = static_cast<int8_t>(dx);
-    sd[1][threadIdx.x] = static_cast<int8_t>(dy);
-    sd[2][threadIdx.x] = static_cast<int8_t>(dz);
     soff[threadIdx.x] = g.off[threadIdx.x];
+    sloc[threadIdx.x] = dx + (dy << TL::LX) + (dz << (TL::LX + TL::LY));
+    sface[threadIdx.x] = (dx < 0 ? 1u : 0u) | (dx > 0 ? 2u : 0u) | (dy < 0 ? 4u : 0u) | (dy > 0 ? 8u : 0u) |
+                         (dz < 0 ? 16u : 0u) | (dz > 0 ? 32u : 0u);
+    shalo[threadIdx.x] = dx + (TL::TX + 2) * (dy + (TL::TY + 2) * dz);
   }
   const uint32_t ntx = (g.X + TL::TX - 1) / TL::TX;
   const uint32_t nty = (g.Y + TL::TY - 1) / TL::TY;
@@ -1270,6 +1277,8 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
   const int ey = min(TL::TY, static_cast<int>(g.Y - y0));
   const int ez = DIM == 2 ? 1 : min(TL::TZ, static_cast<int>(g.Z - z0));
   const uint32_t base = x0 + g.X * y0 + g.XY * z0;
+  for (int r = threadIdx.x; r < NROW; r += kLabelTileThreads)
+    rowbase[r] = base + g.X * (r & (TL::TY - 1)) + g.XY * (r / TL::TY);
   const bool full = ex == TL::TX && ey == TL::TY && ez == TL::TZ;
   // dir tile: 16-byte vector loads when rows are 16-byte aligned and whole
   if (full && (g.X % 16) == 0) {
@@ -1294,22 +1303,16 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
   for (int j = 0; j < PER; ++j) {
     const int i = threadIdx.x + j * kLabelTileThreads;
     const int lx = i & (TL::TX - 1), ly = (i >> TL::LX) & (TL::TY - 1), lz = i >> (TL::LX + TL::LY);
-    const bool val = lx < ex && ly < ey && lz < ez;
     const uint32_t code = sdir[i];
-    uint32_t pr = static_cast<uint32_t>(i) | (static_cast<uint32_t>(i) << 16);
-    if (val) {
-#pragma unroll
-      for (int fam = 0; fam < 2; ++fam) {
-        const uint32_t c = (code >> (4 * fam)) & 15u;
-        if (c == kSelf) continue;
-        const int nx = lx + sd[0][c], ny = ly + sd[1][c], nz = lz + sd[2][c];
-        if (nx >= 0 && nx < ex && ny >= 0 && ny < ey && nz >= 0 && nz < ez) {
-          const uint32_t p = nx + (ny << TL::LX) + (nz << (TL::LX + TL::LY));
-          pr = fam ? ((pr & 0xFFFFu) | (p << 16)) : ((pr & 0xFFFF0000u) | p);
-        }
-      }
-    }
-    ptr[i] = pr;
+    // faces of the (partial) tile this element lies on; outside elements stay put
+    const uint32_t on = (lx < ex && ly < ey && lz < ez)
+                            ? ((lx == 0 ? 1u : 0u) | (lx == ex - 1 ? 2u : 0u) | (ly == 0 ? 4u : 0u) |
+                               (ly == ey - 1 ? 8u : 0u) | (lz == 0 ? 16u : 0u) | (lz == ez - 1 ? 32u : 0u))
+                            : 63u;
+    const uint32_t ca = code & 15u, cd = code >> 4;
+    const uint32_t pa = (sface[ca] & on) ? i : i + sloc[ca];  // SELF: sloc 0
+    const uint32_t pd = (sface[cd] & on) ? i : i + sloc[cd];
+    ptr[i] = pa | (pd << 16);
   }
   __syncthreads();
   // in-place doubling on both families at once
@@ -1327,32 +1330,66 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
     }
     if (!__syncthreads_or(changed)) break;
   }
-  // provisional labels (root, or first vertex outside the tile) + the exits
+  // provisional labels (root, or first vertex outside the tile) + the exits:
+  // the chain's last inside vertex t is a root (code SELF) or steps out by
+  // slot c, so the label is gid(t) + soff[c] (soff[SELF] = 0)
 #pragma unroll
   for (int j = 0; j < PER; ++j) {
     const int i = threadIdx.x + j * kLabelTileThreads;
     const int lx = i & (TL::TX - 1), ly = (i >> TL::LX) & (TL::TY - 1), lz = i >> (TL::LX + TL::LY);
     if (lx < ex && ly < ey && lz < ez) {
       const uint32_t p = ptr[i];
-      const uint32_t gi = base + lx + g.X * ly + g.XY * lz;
+      const uint32_t gi = rowbase[i >> TL::LX] + lx;
 #pragma unroll
       for (int fam = 0; fam < 2; ++fam) {
         const int t = fam ? (p >> 16) : (p & 0xFFFFu);
         const uint32_t c = (sdir[t] >> (4 * fam)) & 15u;
-        const int tlx = t & (TL::TX - 1), tly = (t >> TL::LX) & (TL::TY - 1),
-                  tlz = t >> (TL::LX + TL::LY);
-        const uint32_t res = base + tlx + g.X * tly + g.XY * tlz + soff[c];  // soff[15] = 0
+        const uint32_t res = rowbase[t >> TL::LX] + (t & (TL::TX - 1)) + soff[c];
         (fam ? m : M)[gi] = res;
         // fin is only ever read at provisional-label values: roots (here) and
         // exits (seeded by k_exit_reset), so non-roots need no fin write
         if (res == gi) (fam ? finm : finM)[gi] = res;
-        if (t == i && c != kSelf) {
-          const int hx = tlx + sd[0][c] + 1, hy = tly + sd[1][c] + 1;
-          const int hz = DIM == 2 ? 0 : tlz + sd[2][c] + 1;
-          const int h = hx + (TL::TX + 2) * (hy + (TL::TY + 2) * hz);
-          if (!(atomicOr(&seen[fam][h >> 5], 1u << (h & 31)) & (1u << (h & 31))))
-            sexit[fam][atomicAdd(&sexit_n[fam], 1u)] = res;
-        }
+      }
+    }
+  }
+  // the tile's distinct exits: only surface elements can step out, so walk the
+  // six faces (edges/corners repeat; the halo bitmap dedupes) with full warps
+  {
+    constexpr int NFX = TL::TY * TL::TZ, NFY = TL::TX * TL::TZ, NFZ = DIM == 2 ? 0 : TL::TX * TL::TY;
+    constexpr int NF = 2 * (NFX + NFY + NFZ);
+    for (int k = threadIdx.x; k < NF; k += kLabelTileThreads) {
+      int lx, ly, lz, q = k;
+      if (q < 2 * NFX) {
+        lx = q < NFX ? 0 : ex - 1;
+        q %= NFX;
+        ly = q % TL::TY;
+        lz = q / TL::TY;
+      } else if ((q -= 2 * NFX) < 2 * NFY) {
+        ly = q < NFY ? 0 : ey - 1;
+        q %= NFY;
+        lx = q % TL::TX;
+        lz = q / TL::TX;
+      } else {
+        q -= 2 * NFY;
+        lz = q < NFZ ? 0 : ez - 1;
+        q %= NFZ;
+        lx = q % TL::TX;
+        ly = q / TL::TX;
+      }
+      if (lx >= ex || ly >= ey || lz >= ez) continue;
+      const int i = lx + (ly << TL::LX) + (lz << (TL::LX + TL::LY));
+      const uint32_t code = sdir[i];
+      const uint32_t on = (lx == 0 ? 1u : 0u) | (lx == ex - 1 ? 2u : 0u) | (ly == 0 ? 4u : 0u) |
+                          (ly == ey - 1 ? 8u : 0u) | (lz == 0 ? 16u : 0u) | (lz == ez - 1 ? 32u : 0u);
+      const uint32_t gi = rowbase[i >> TL::LX] + lx;
+      const int hb = (lx + 1) + (TL::TX + 2) * ((ly + 1) + (TL::TY + 2) * (DIM == 2 ? 0 : lz + 1));
+#pragma unroll
+      for (int fam = 0; fam < 2; ++fam) {
+        const uint32_t c = (code >> (4 * fam)) & 15u;
+        if (!(sface[c] & on)) continue;  // SELF or a step inside the tile
+        const int h = hb + shalo[c];
+        if (!(atomicOr(&seen[fam][h >> 5], 1u << (h & 31)) & (1u << (h & 31))))
+          sexit[fam][atomicAdd(&sexit_n[fam], 1u)] = gi + soff[c];
       }
     }
   }
