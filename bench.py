@@ -44,17 +44,20 @@ sys.path.insert(0, ROOT)
 METRIC = "Mvertices/s end-to-end correction (to convergence)"
 UNIT = "Mvertices/s"
 
-# algorithmic bytes per vertex per launch (f32 values)
-def alg_bytes_per_vertex(cls: str, es: int) -> float:
+# Algorithmic bytes of the timed steps per kernel class, from the
+# step's own counters where a launch covers less than the whole field.  Classes
+# without an entry (persistent subloop, gathers over lists) are latency-bound
+# and not roofline-graded.
+def alg_bytes(cls: str, es: int, n: int, st, launches: int) -> float:
+    tile = 8192
     return {
-        "validate": 2 * es,
-        "directions": es + 1,
-        "detect_kind": 2,
-        "detect_all": 2,
-        "label_init": 1 + 8,      # k_label_tile: dir byte in, two u32 labels out
-        "label_finish": 8 + 8,    # read both labels + one gather each (writes only if changed)
-        "rfix": 2 + 16,
-        "compact": 2,
+        "validate": 2 * es * n * launches,               # read f and fhat
+        "directions": (es + 1) * n * launches,           # read values, write one code byte
+        "detect_kind": 2 * n * launches,                 # full sweeps: fdir + gdir
+        "label_init": 9 * tile * st.label_tiles,         # code byte in, two u32 labels out per tile vertex
+        "label_finish": 16 * n * launches,               # two labels read + gathered (f labels once)
+        "rfix": 2 * tile * st.rfix_tiles,                # lower bound: both codes of every listed tile vertex
+        "compact": 2 * n * launches,                     # flag sweep (count + write passes)
     }.get(cls, 0.0)
 
 
@@ -349,18 +352,34 @@ def main():
                 agg[name]["ms"] += d["ms"]
         prof = {k: {"launches": v["launches"] // len(stats), "ms": v["ms"] / len(stats)}
                 for k, v in agg.items() if v["launches"]}
-        graded = {k: v for k, v in agg.items() if alg_bytes_per_vertex(k, es) and v["launches"]}
+        graded = {}
+        for k, v in agg.items():
+            if not v["launches"]:
+                continue
+            tot = sum(alg_bytes(k, es, n_local, s, s.kernel_profile()[k]["launches"]) for s in stats)
+            if tot:
+                graded[k] = {"launches": v["launches"], "ms": v["ms"], "bytes": tot,
+                             "achieved_GBps": tot / (v["ms"] * 1e-3) / 1e9}
         top = max(graded, key=lambda k: graded[k]["ms"])
         per_launch_ms = graded[top]["ms"] / graded[top]["launches"]
-        bytes_per_launch = alg_bytes_per_vertex(top, es) * n_local
-        achieved = bytes_per_launch / (per_launch_ms * 1e-3) / 1e9
+        bytes_per_launch = graded[top]["bytes"] / graded[top]["launches"]
+        achieved = graded[top]["achieved_GBps"]
         total_ms = sum(v["ms"] for v in agg.values())
+        traffic = None  # measured DRAM bytes per launch of this kernel (committed ncu capture, same config)
+        tpath = os.path.join(ROOT, "profiles", "ncu_traffic_c4.json")
+        if cfg.name == "C4" and dims == cfg.dims and os.path.exists(tpath):
+            with open(tpath) as fp:
+                traffic = (json.load(fp).get(top) or {}).get("dram_bytes_per_launch")
         roofline = {"kernel": top, "bound": "hbm", "achieved": achieved, "peak": peak,
-                    "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                    "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                     "peak_source": peak_src,
                     "alg_bytes_per_launch": bytes_per_launch,
                     "mean_launch_us": per_launch_ms * 1e3,
-                    "share_of_device_time": graded[top]["ms"] / total_ms if total_ms else None}
+                    "share_of_device_time": graded[top]["ms"] / total_ms if total_ms else None,
+                    "per_class": {k: {"launches_per_step": v["launches"] // len(stats),
+                                      "ms_per_step": v["ms"] / len(stats),
+                                      "achieved_GBps": v["achieved_GBps"],
+                                      "frac": v["achieved_GBps"] / peak} for k, v in graded.items()}}
 
     # ---- verification report of the corrected field, device-resident
     verify = None

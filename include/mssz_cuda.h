@@ -89,6 +89,7 @@ typedef struct mssz_cu_options {
 #define MSSZ_CU_PROF_LABEL_FINISH 10
 #define MSSZ_CU_PROF_FIX 11 /* host-driven huge batch: fix_list */
 #define MSSZ_CU_PROF_SPARSE 12 /* sparse R iteration kernels */
+#define MSSZ_CU_PROF_DETECT_DIRTY 13 /* subloop detection over changed chunks (k_detect_dirty) */
 #define MSSZ_CU_PROF_CLASSES 16
 
 /* Mirrors EditStats (edit_engine.hpp:54-68) field for field, then adds the

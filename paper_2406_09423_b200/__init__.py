@@ -262,7 +262,8 @@ class _Stats(C.Structure):
 
 _ARRAY_FIELDS = ("sub_iterations", "kernel_count", "kernel_ms")
 PROF_CLASSES = ["validate", "directions", "detect_kind", "detect_all", "subloop", "label_init",
-                "label_jump", "rfix", "frontier", "compact", "label_finish", "fix", "sparse"]
+                "label_jump", "rfix", "frontier", "compact", "label_finish", "fix", "sparse",
+                "detect_dirty"]
 
 
 _BATCH_CB = C.CFUNCTYPE(None, C.c_void_p, C.c_uint64, C.c_void_p)

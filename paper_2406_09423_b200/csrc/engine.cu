@@ -302,6 +302,7 @@ enum {
   kProfLabelFinish = MSSZ_CU_PROF_LABEL_FINISH,
   kProfFix = MSSZ_CU_PROF_FIX,
   kProfSparse = MSSZ_CU_PROF_SPARSE,
+  kProfDetectDirty = MSSZ_CU_PROF_DETECT_DIRTY,
 };
 
 // ---------------------------------------------------------------------------
@@ -703,14 +704,15 @@ struct Engine {
   uint64_t run_subloop(int kind) {
     reset_ctl();
     ws.push_ctl();
-    pre(kProfDetectKind);
+    const int dcls = fresh[kind] ? kProfDetectDirty : kProfDetectKind;
+    pre(dcls);
     if (fresh[kind])
       k_detect_dirty<<<grid_for((n() + 15) / 16, 256, ws.sms, 16), 256, 0, ws.stream>>>(
           s.fdir, s.gdir, n(), s.cstamp, end_mark[kind], kind, s.list[cur], &ws.ctl->list_count[cur]);
     else
       k_detect_kind<<<grid_for((n() + 15) / 16, 256, ws.sms, 16), 256, 0, ws.stream>>>(
           s.fdir, s.gdir, n(), kind, s.list[cur], &ws.ctl->list_count[cur]);
-    launched(kProfDetectKind);
+    launched(dcls);
     ++st.detect_sweeps;
     const uint32_t batch_base = ws.next_batch, mark_base = ws.next_mark;
     // stamp ids must never be reused, also when this subloop raises
