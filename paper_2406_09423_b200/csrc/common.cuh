@@ -296,6 +296,38 @@ __device__ __forceinline__ void WarpBuffer<K>::flush(uint32_t* __restrict__ list
   n = 0;
 }
 
+// Block-wide reservation: every thread of the block calls it (block-uniform
+// control flow) with its count c; one atomic per block instead of one per warp,
+// so long appends from full sweeps do not serialise on the counter.
+__device__ __forceinline__ uint32_t block_reserve(uint32_t c, uint32_t* count) {
+  __shared__ uint32_t wsum[32];
+  __shared__ uint32_t bbase;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  uint32_t incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    const uint32_t v = lane < nw ? wsum[lane] : 0u;
+    uint32_t s = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += t;
+    }
+    if (lane < nw) wsum[lane] = s - v;  // exclusive warp offsets
+    if (lane == 31) bbase = s ? atomicAdd(count, s) : 0u;
+  }
+  __syncthreads();
+  const uint32_t base = bbase + wsum[w] + incl - c;
+  __syncthreads();  // wsum / bbase are reused by the next call
+  return base;
+}
+
 constexpr int kStageK = 4;
 constexpr int kStageWarps = 16;  // blocks of up to 512 threads
 // per-warp staging slice of a [kStageWarps][kStageK * 32] shared array

@@ -865,8 +865,9 @@ __device__ __forceinline__ void detect_chunks(const uint8_t* __restrict__ fdir,
                                               int kind, uint32_t* __restrict__ list,
                                               uint32_t* count, uint64_t tid, uint64_t stride) {
   const uint64_t nchunks = (static_cast<uint64_t>(n) + 15) / 16;
-  for (uint64_t wb = tid & ~uint64_t(31); wb < nchunks; wb += stride) {
-    const uint64_t c = wb + (threadIdx.x & 31);
+  // block-uniform trip count (block_reserve)
+  for (uint64_t bb = tid - threadIdx.x; bb < nchunks; bb += stride) {
+    const uint64_t c = bb + threadIdx.x;
     uint32_t mask = 0;
     if (c < nchunks) {
       const uint64_t v0 = c * 16;
@@ -883,8 +884,8 @@ __device__ __forceinline__ void detect_chunks(const uint8_t* __restrict__ fdir,
             mask |= 1u << j;
       }
     }
-    const uint32_t base = warp_reserve(__popc(mask), count);
-    uint32_t pos = base;
+    if (!__syncthreads_or(mask != 0)) continue;
+    uint32_t pos = block_reserve(__popc(mask), count);
     while (mask) {
       const int j = __ffs(mask) - 1;
       mask &= mask - 1;
@@ -920,31 +921,49 @@ __global__ void __launch_bounds__(256) k_detect_dirty(const uint8_t* __restrict_
                                                       const uint32_t* __restrict__ cstamp, uint32_t since,
                                                       int kind, uint32_t* __restrict__ list,
                                                       uint32_t* count) {
-  const uint64_t nq = (static_cast<uint64_t>(n) + 15) / 16;  // 16-vertex groups, 4 per chunk
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t wb = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) & ~uint64_t(31); wb < nq;
-       wb += stride) {
-    const uint64_t q = wb + (threadIdx.x & 31);
-    uint32_t mask = 0;
-    if (q < nq && __ldg(cstamp + (q >> 2)) >= since) {
-      const uint64_t v0 = q * 16;
-      if (v0 + 16 <= n) {
-        const uint4 f = __ldg(reinterpret_cast<const uint4*>(fdir + v0));
-        const uint4 g = __ldg(reinterpret_cast<const uint4*>(gdir + v0));
-        mask = bytes_to_nibble(kind_bytes(kind, f.x, g.x)) | bytes_to_nibble(kind_bytes(kind, f.y, g.y)) << 4 |
-               bytes_to_nibble(kind_bytes(kind, f.z, g.z)) << 8 | bytes_to_nibble(kind_bytes(kind, f.w, g.w)) << 12;
-      } else {
-        for (int j = 0; j < 16; ++j)
-          if (v0 + j < n && kind_match(kind, fdir[v0 + j], gdir[v0 + j])) mask |= 1u << j;
-      }
+  // warp-centric: a warp ballots the stamps of 4 x 32 consecutive chunks (all
+  // loads in flight at once), then scans its dirty chunks 8 at a time, four
+  // lanes x 16 vertices per chunk
+  const uint32_t nch = (n + 63) / 64;
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t c0 = gw * 128; c0 < nch; c0 += nw * 128) {
+    uint32_t st[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      const uint64_t c = c0 + g * 32 + lane;
+      st[g] = c < nch ? __ldg(cstamp + c) : 0u;
     }
-    if (!__any_sync(0xffffffffu, mask != 0)) continue;
-    const uint32_t base = warp_reserve(__popc(mask), count);
-    uint32_t pos = base;
-    while (mask) {
-      const int j = __ffs(mask) - 1;
-      mask &= mask - 1;
-      list[pos++] = static_cast<uint32_t>(q * 16 + j);
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      const uint32_t bits = __ballot_sync(0xffffffffu, st[g] >= since && c0 + g * 32 + lane < nch);
+      const int nd = __popc(bits);
+      for (int b0 = 0; b0 < nd; b0 += 8) {
+        const int k = b0 + (lane >> 2);
+        uint32_t mask = 0;
+        uint64_t v0 = 0;
+        if (k < nd) {
+          const uint64_t c = c0 + g * 32 + __fns(bits, 0, k + 1);
+          v0 = c * 64 + (lane & 3) * 16;
+          if (v0 + 16 <= n) {
+            const uint4 f = __ldg(reinterpret_cast<const uint4*>(fdir + v0));
+            const uint4 gg = __ldg(reinterpret_cast<const uint4*>(gdir + v0));
+            mask = bytes_to_nibble(kind_bytes(kind, f.x, gg.x)) | bytes_to_nibble(kind_bytes(kind, f.y, gg.y)) << 4 |
+                   bytes_to_nibble(kind_bytes(kind, f.z, gg.z)) << 8 |
+                   bytes_to_nibble(kind_bytes(kind, f.w, gg.w)) << 12;
+          } else {
+            for (int j = 0; j < 16; ++j)
+              if (v0 + j < n && kind_match(kind, fdir[v0 + j], gdir[v0 + j])) mask |= 1u << j;
+          }
+        }
+        uint32_t pos = warp_reserve(__popc(mask), count);
+        while (mask) {
+          const int j = __ffs(mask) - 1;
+          mask &= mask - 1;
+          list[pos++] = static_cast<uint32_t>(v0 + j);
+        }
+      }
     }
   }
 }
