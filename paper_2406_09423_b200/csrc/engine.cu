@@ -274,7 +274,7 @@ Workspace& workspace(int device) {
 }
 
 // worklists up to this size run inside the leader CTA of k_subloop
-constexpr uint32_t kSmallBatchMax = 4096;
+uint32_t kSmallBatchMax = 256;  // tunable via MSSZ_SMALL_MAX (experiments)
 // worklists above n / kHugeBatchDivisor are run by host-launched streaming kernels
 uint32_t kHugeBatchDivisor = 64;  // tunable via MSSZ_HUGE_DIVISOR (experiments)
 // R batches applying more than n / kRHugeDivisor edits refresh with a full sweep
@@ -628,6 +628,7 @@ struct Engine {
     if (coop_blocks) return coop_blocks;
     if (const char* h = std::getenv("MSSZ_HUGE_DIVISOR")) kHugeBatchDivisor = std::max(1, std::atoi(h));
     if (const char* h = std::getenv("MSSZ_RHUGE_DIVISOR")) kRHugeDivisor = std::max(1, std::atoi(h));
+    if (const char* h = std::getenv("MSSZ_SMALL_MAX")) kSmallBatchMax = static_cast<uint32_t>(std::max(0, std::atoi(h)));
     if (const char* h = std::getenv("MSSZ_SPARSE_DIVISOR")) kSparseMismDivisor = std::max(1, std::atoi(h));
     int occ = 0;
     if (geo.ndims == 2)
