@@ -148,7 +148,7 @@ struct Workspace {
   int device = 0;
   int sms = 0;
   cudaStream_t stream = nullptr;
-  DevBuf f, g, fdir, gdir, touched, stamp, fmark, lab, fin, lists, tiles;
+  DevBuf f, g, fh, fdir, gdir, touched, stamp, fmark, lab, fin, lists, tiles;
   DevBuf tE, tEcnt, toldfin, tdirty, taffected, tbits, tcnt, tlist;  // label-tile store
   DevBuf xbuf;  // sparse R pass: crossing lists X (2 families x 2 buffers)
   DevBuf cbits; // 1 bit per 64-vertex chunk whose direction codes changed
@@ -201,7 +201,7 @@ struct Workspace {
     stream = nullptr;
   }
   void release() {
-    for (DevBuf* b : {&f, &g, &fdir, &gdir, &touched, &stamp, &fmark, &lab, &fin, &lists, &tiles,
+    for (DevBuf* b : {&f, &g, &fh, &fdir, &gdir, &touched, &stamp, &fmark, &lab, &fin, &lists, &tiles,
                       &tE, &tEcnt, &toldfin, &tdirty, &taffected, &tbits, &tcnt, &tlist, &xbuf, &cbits, &cstamp})
       b->release();
     next_batch = next_mark = 1;
@@ -330,6 +330,8 @@ struct Engine {
   uint32_t end_mark[4] = {0, 0, 0, 0};
   bool fresh[4] = {false, false, false, false};
   float dir_ms = 0.f, lab_ms = 0.f;
+
+  const T* fhat = nullptr;  // decompressed input on the device (derives touched at compaction)
 
   Engine(Workspace& w, const Geom& g, const mssz_cu_options& o) : ws(w), geo(g), opt(o) {}
 
@@ -1039,7 +1041,7 @@ struct Engine {
     st.input_bound_violations = violations;
 
     // EditState ctor (edit_engine.cpp:36-56)
-    CK(cudaMemsetAsync(s.touched, 0, n(), ws.stream));
+    s.touched = nullptr;  // touched == (g != fhat), derived by edit_flags()
     CK(cudaEventRecord(ws.ev[0], ws.stream));
     directions(d_f, ws.fdir.as<uint8_t>());
     directions(s.g, s.gdir);
@@ -1101,6 +1103,15 @@ struct Engine {
     return total;
   }
 
+  // EditSet membership (edit_engine.cpp:368-378): g != fhat, into ws.touched
+  const uint8_t* edit_flags() {
+    uint8_t* flag = ws.touched.as<uint8_t>();
+    pre(kProfCompact);
+    k_flag_changed<T><<<grid_for(n() / 4 + 1, 256, ws.sms, 8), 256, 0, ws.stream>>>(s.g, fhat, n(), flag);
+    launched(kProfCompact);
+    return flag;
+  }
+
   // device EditSet buffers inside the (now idle) worklist block
   uint64_t* edit_idx() const { return reinterpret_cast<uint64_t*>(ws.lists.p); }
   T* edit_val() const {
@@ -1153,11 +1164,14 @@ void derive_host(int ndims, const uint64_t* dims, const T* f, const T* fh, doubl
   cudaEvent_t evs[4] = {t0, t1, t2, t3};
   EvGuard guard{evs};
   CK(cudaEventRecord(t0, ws.stream));
+  ws.fh.ensure(sizeof(T) * ((geo.n + 63) & ~uint64_t(63)));
   CK(cudaMemcpyAsync(ws.f.p, f, sizeof(T) * geo.n, cudaMemcpyHostToDevice, ws.stream));
-  CK(cudaMemcpyAsync(ws.g.p, fh, sizeof(T) * geo.n, cudaMemcpyHostToDevice, ws.stream));
+  CK(cudaMemcpyAsync(ws.fh.p, fh, sizeof(T) * geo.n, cudaMemcpyHostToDevice, ws.stream));
+  CK(cudaMemcpyAsync(ws.g.p, ws.fh.p, sizeof(T) * geo.n, cudaMemcpyDeviceToDevice, ws.stream));
   CK(cudaEventRecord(t1, ws.stream));
+  eng.fhat = ws.fh.as<T>();
   eng.run(ws.f.as<T>(), xi);
-  const uint64_t count = eng.compact(eng.s.touched, 1, eng.s.g, eng.edit_idx(), eng.edit_val());
+  const uint64_t count = eng.compact(eng.edit_flags(), 1, eng.s.g, eng.edit_idx(), eng.edit_val());
   CK(cudaEventRecord(t2, ws.stream));
   uint64_t* hi = idx_buf;
   T* hv = val_buf;
@@ -1214,8 +1228,9 @@ void derive_device(int ndims, const uint64_t* dims, const T* d_f, const T* d_fh,
   CK(cudaEventCreate(&t1));
   CK(cudaEventRecord(t0, ws.stream));
   CK(cudaMemcpyAsync(ws.g.p, d_fh, sizeof(T) * geo.n, cudaMemcpyDeviceToDevice, ws.stream));
+  eng.fhat = d_fh;
   eng.run(d_f, xi);
-  const uint64_t count = eng.compact(eng.s.touched, 1, eng.s.g, eng.edit_idx(), eng.edit_val());
+  const uint64_t count = eng.compact(eng.edit_flags(), 1, eng.s.g, eng.edit_idx(), eng.edit_val());
   if (count > capacity) {
     *count_out = count;
     cudaEventDestroy(t0);

@@ -656,7 +656,7 @@ __device__ __forceinline__ bool claim_and_lower(const State<T>& s, uint32_t t, u
   T nv;
   if (!lower_value<T>(__ldcg(s.g + t), __ldg(s.f + t), s.xi, nv)) return false;
   s.g[t] = nv;
-  s.touched[t] = 1;
+  if (s.touched) s.touched[t] = 1;
   return true;
 }
 
@@ -704,7 +704,7 @@ __device__ __forceinline__ void fix_batch(const State<T>& s, const uint32_t* __r
       T nv;
       if (prev[j] != batch && lower_value<T>(gv[j], fv[j], s.xi, nv)) {
         s.g[t[j]] = nv;
-        s.touched[t[j]] = 1;
+        if (s.touched) s.touched[t[j]] = 1;  // single device: derived at compaction
         ok[j] = true;
       }
     }
@@ -2028,6 +2028,28 @@ __global__ void __launch_bounds__(256) k_validate(const T* __restrict__ f,
     if (bad) atomicAdd(reinterpret_cast<unsigned long long*>(&ctl->nonfinite), (unsigned long long)bad);
     if (viol) atomicAdd(reinterpret_cast<unsigned long long*>(&ctl->violations), (unsigned long long)viol);
   }
+}
+
+// touched == (g != fhat) bitwise: every successful lower_step strictly lowers
+// g (edit_engine.cpp:75-86), so the single-device engine keeps no touched
+// array (one random line less per edit) and derives it here before K6.
+template <class T>
+__global__ void __launch_bounds__(256) k_flag_changed(const T* __restrict__ g, const T* __restrict__ fh,
+                                                      uint64_t n, uint8_t* __restrict__ flag) {
+  using B = typename KeyOf<T>::type;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t n4 = n / 4;
+  for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n4; q += stride) {
+    uint32_t f4 = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const B a = reinterpret_cast<const B*>(g)[q * 4 + j], b = __ldg(reinterpret_cast<const B*>(fh) + q * 4 + j);
+      f4 |= (a != b ? 1u : 0u) << (8 * j);
+    }
+    reinterpret_cast<uint32_t*>(flag)[q] = f4;
+  }
+  for (uint64_t v = n4 * 4 + static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride)
+    flag[v] = reinterpret_cast<const B*>(g)[v] != reinterpret_cast<const B*>(fh)[v] ? 1 : 0;
 }
 
 // ---------------------------------------------------------------------------
