@@ -364,7 +364,6 @@ struct Engine {
     s.cstamp = ws.cstamp.as<uint32_t>();
     s.own_lo = s.act_lo = 0;
     s.own_n = s.act_n = geo.n;
-    s.tune = std::getenv("MSSZ_TUNE") ? static_cast<uint32_t>(std::atoi(std::getenv("MSSZ_TUNE"))) : 0u;
   }
 
   // Per-kernel-class device time (CUDA events on the launching stream), only

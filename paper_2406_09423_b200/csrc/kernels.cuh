@@ -643,7 +643,6 @@ struct State {
   // frontier refreshes only vertices in [act_lo, act_lo + act_n) (owned planes plus
   // one halo plane per side).  Single device: both ranges are the whole grid.
   uint32_t own_lo, own_n, act_lo, act_n;
-  uint32_t tune;  // experiment bits (MSSZ_TUNE): 1 = frontier claims without the pre-check load
   uint32_t* cstamp;  // per 64-vertex chunk: mark id of the last batch that changed a code in it
 };
 
