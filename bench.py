@@ -407,6 +407,20 @@ def main():
                   "false_extrema": [rep.fp_max, rep.fp_min, rep.fn_max, rep.fn_min],
                   "gpu_launches": rep.kernel_launches}
 
+    # ---- base codec on the GPU: the reconstruction producing fhat
+    base_codec = None
+    if not sharded and f is not None:
+        tc, td = {}, {}
+        recon, sym, lits = P.compress_base(topo, f, xi, tc)
+        back = P.decompress_base(topo, sym, lits, xi, dtype, td)
+        base_codec = {"compress_device_ms": tc["device_ms"], "decompress_device_ms": td["device_ms"],
+                      "decompress_value": n / (td["device_ms"] * 1e-3) / 1e6, "unit": UNIT,
+                      "escapes": int(lits.size),
+                      "identical_to_input_fhat": bool(recon.tobytes() == fh.tobytes()),
+                      "round_trip": bool(back.tobytes() == recon.tobytes()),
+                      "api": "mssz_cu_compress_base / mssz_cu_decompress_base (block wavefront)"}
+        del recon, sym, lits, back
+
     # ---- e2e through the host API with pinned buffers
     e2e = None
     if not args.no_e2e:
@@ -477,6 +491,7 @@ def main():
         "cpu_baseline": cpu,
         "e2e": e2e,
         "verify": verify,
+        "base_codec": base_codec,
         "gpu_launches": int(dist.sum(float(sum(s.kernel_launches for s in stats)))),
         "clocks": clk,
         "edit_stats": {"outer_iterations": st.outer_iterations, "c_passes": st.c_passes,

@@ -264,6 +264,23 @@ int mssz_cu_segmentation_f32(int ndims, const uint64_t* dims, const float* value
 int mssz_cu_segmentation_f64(int ndims, const uint64_t* dims, const double* values, uint64_t* max_label,
                              uint64_t* min_label);
 
+/* ---- base codec on the GPU: compress_base / decompress_base ----
+ * compress: values -> reconstruction (the f-hat the correction loop takes) and the
+ *   quantisation symbols (0 = escape, else 1 + zigzag(q)) that huffman::encode_stream
+ *   codes (base_codec.cpp:76-120); literals are the values at symbol-0 positions in
+ *   index order.  decompress: (symbols, literals) after huffman::decode_stream ->
+ *   reconstruction (base_codec.cpp:122-152).  Bit-exact with the reference (Lorenzo
+ *   order-1 prediction, double arithmetic, block wavefront).  device_ms (nullable):
+ *   device time of the wavefront. */
+int mssz_cu_compress_base_f32(int ndims, const uint64_t* dims, const float* values, double xi, float* recon,
+                              uint32_t* symbols /* nullable */, uint64_t* escapes, double* device_ms);
+int mssz_cu_compress_base_f64(int ndims, const uint64_t* dims, const double* values, double xi, double* recon,
+                              uint32_t* symbols /* nullable */, uint64_t* escapes, double* device_ms);
+int mssz_cu_decompress_base_f32(int ndims, const uint64_t* dims, const uint32_t* symbols, const float* literals,
+                                uint64_t n_literals, double xi, float* recon, double* device_ms);
+int mssz_cu_decompress_base_f64(int ndims, const uint64_t* dims, const uint32_t* symbols, const double* literals,
+                                uint64_t n_literals, double xi, double* recon, double* device_ms);
+
 #ifdef __cplusplus
 }
 #endif

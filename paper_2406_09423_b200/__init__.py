@@ -34,6 +34,7 @@ __all__ = [
     "detect_kind", "lower_step", "representable_floor", "apply_edits", "segmentation_equal",
     "library", "build", "slab_range", "derive_edits_slabs", "SlabComm",
     "VerificationReport", "build_report", "build_report_device", "segmentation", "export_labels",
+    "compress_base", "decompress_base",
 ]
 
 FPMAX, FPMIN, FNMAX, FNMIN = 0, 1, 2, 3
@@ -279,7 +280,8 @@ EXPORTS = [
         "derive_edits", "derive_edits_into", "derive_edits_device", "compute_directions",
         "compute_direction_codes", "detect_false_critical", "detect_kind", "lower_step",
         "representable_floor", "apply_edits", "derive_edits_slab", "derive_edits_slab_device",
-        "derive_edits_slabs_local", "verify", "verify_device", "segmentation")
+        "derive_edits_slabs_local", "verify", "verify_device", "segmentation", "compress_base",
+        "decompress_base")
 ]
 
 _lib = None
@@ -744,3 +746,40 @@ def export_labels(labels: SegmentationLabels, path: str) -> None:
     with open(path, "wb") as fp:
         fp.write(np.ascontiguousarray(labels.max_label, "<u8").tobytes())
         fp.write(np.ascontiguousarray(labels.min_label, "<u8").tobytes())
+
+
+# ---------------------------------------------------------------- base codec (GPU)
+def compress_base(topo: GridTopology, values, xi: float, timing: Optional[dict] = None):
+    """compress_base<T> (base_codec.cpp:76-120) on the GPU -> (reconstruction, symbols,
+    literals): symbols are what huffman::encode_stream codes (0 = escape, else
+    1 + zigzag(q)), literals the escaped values in index order."""
+    v = _field(topo, values, "values")
+    recon = np.empty_like(v)
+    sym = np.empty(topo.vertex_count, np.uint32)
+    esc = C.c_uint64()
+    ms = C.c_double()
+    _check(getattr(library(), f"mssz_cu_compress_base_{_suf(v.dtype)}")(
+        topo.ndims, _dims(topo), _p(v), C.c_double(xi), _p(recon), _p(sym), C.byref(esc),
+        C.byref(ms)))
+    if timing is not None:
+        timing["device_ms"] = ms.value
+    lits = v[sym == 0]
+    assert lits.size == esc.value
+    return recon, sym, lits
+
+
+def decompress_base(topo: GridTopology, symbols, literals, xi: float, dtype=np.float32,
+                    timing: Optional[dict] = None) -> np.ndarray:
+    """decompress_base<T> (base_codec.cpp:122-152) after the Huffman decode, on the GPU."""
+    sym = np.ascontiguousarray(symbols, np.uint32).reshape(-1)
+    if sym.size != topo.vertex_count:
+        raise Error(ErrKind.corrupt_archive, "code count does not match the grid")
+    lit = np.ascontiguousarray(literals, dtype).reshape(-1)
+    out = np.empty(topo.vertex_count, dtype)
+    ms = C.c_double()
+    _check(getattr(library(), f"mssz_cu_decompress_base_{_suf(dtype)}")(
+        topo.ndims, _dims(topo), _p(sym), _p(lit) if lit.size else None, C.c_uint64(lit.size),
+        C.c_double(xi), _p(out), C.byref(ms)))
+    if timing is not None:
+        timing["device_ms"] = ms.value
+    return out

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <limits>
 #include <chrono>
@@ -1601,3 +1602,4 @@ int mssz_cu_classify_critical(uint64_t n, const uint64_t* asc, const uint64_t* d
 
 #include "shard_api.cuh"
 #include "verify.cuh"
+#include "base_codec.cuh"
