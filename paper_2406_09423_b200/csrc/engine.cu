@@ -711,7 +711,7 @@ struct Engine {
     pre(dcls);
     if (fresh[kind])
       k_detect_dirty<<<grid_for((n() + 15) / 16, 256, ws.sms, 16), 256, 0, ws.stream>>>(
-          s.fdir, s.gdir, n(), s.cstamp, end_mark[kind], kind, s.list[cur], &ws.ctl->list_count[cur]);
+          s.fdir, s.gdir, n(), s.cstamp, end_mark[kind], kind, s.list[cur], &ws.ctl->list_count[cur], 0u, n());
     else
       k_detect_kind<<<grid_for((n() + 15) / 16, 256, ws.sms, 16), 256, 0, ws.stream>>>(
           s.fdir, s.gdir, n(), kind, s.list[cur], &ws.ctl->list_count[cur]);

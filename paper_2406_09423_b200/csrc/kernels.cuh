@@ -915,11 +915,12 @@ __global__ void __launch_bounds__(256) k_detect_kind(const uint8_t* __restrict__
 // mark `since` (cstamp[c] >= since).  At the end of a subloop its kind's list
 // is empty, and a vertex can only change class when its g-direction changes,
 // so at the kind's next subloop these chunks hold every item.
+// [lo, hi): vertex range kept (z-slab sharding: the active range of a window)
 __global__ void __launch_bounds__(256) k_detect_dirty(const uint8_t* __restrict__ fdir,
                                                       const uint8_t* __restrict__ gdir, uint32_t n,
                                                       const uint32_t* __restrict__ cstamp, uint32_t since,
                                                       int kind, uint32_t* __restrict__ list,
-                                                      uint32_t* count) {
+                                                      uint32_t* count, uint32_t lo, uint32_t hi) {
   // warp-centric: a warp ballots the stamps of 4 x 32 consecutive chunks (all
   // loads in flight at once), then scans its dirty chunks 8 at a time, four
   // lanes x 16 vertices per chunk
@@ -945,7 +946,7 @@ __global__ void __launch_bounds__(256) k_detect_dirty(const uint8_t* __restrict_
         if (k < nd) {
           const uint64_t c = c0 + g * 32 + __fns(bits, 0, k + 1);
           v0 = c * 64 + (lane & 3) * 16;
-          if (v0 + 16 <= n) {
+          if (v0 >= lo && v0 + 16 <= hi) {
             const uint4 f = __ldg(reinterpret_cast<const uint4*>(fdir + v0));
             const uint4 gg = __ldg(reinterpret_cast<const uint4*>(gdir + v0));
             mask = bytes_to_nibble(kind_bytes(kind, f.x, gg.x)) | bytes_to_nibble(kind_bytes(kind, f.y, gg.y)) << 4 |
@@ -953,7 +954,7 @@ __global__ void __launch_bounds__(256) k_detect_dirty(const uint8_t* __restrict_
                    bytes_to_nibble(kind_bytes(kind, f.w, gg.w)) << 12;
           } else {
             for (int j = 0; j < 16; ++j)
-              if (v0 + j < n && kind_match(kind, fdir[v0 + j], gdir[v0 + j])) mask |= 1u << j;
+              if (v0 + j >= lo && v0 + j < hi && kind_match(kind, fdir[v0 + j], gdir[v0 + j])) mask |= 1u << j;
           }
         }
         uint32_t pos = warp_reserve(__popc(mask), count);

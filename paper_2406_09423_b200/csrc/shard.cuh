@@ -717,11 +717,21 @@ struct SlabEngine {
     return n_lo + n_hi;
   }
 
-  void detect(int kind, uint32_t* list, uint32_t* count) {
-    eng.pre(kProfDetectKind);
-    k_detect_range<<<blocks((act_hi - act_lo) / 16 + 1, 16), 256, 0, ws.stream>>>(
-        s().fdir, s().gdir, act_lo, act_hi, kind, list, count);
-    eng.launched(kProfDetectKind);
+  // full sweep, or (kind's list empty since its last subloop, no full direction
+  // sweep since) only the chunks whose codes changed (see Engine::run_subloop)
+  void detect(int kind, uint32_t* list, uint32_t* count, bool allow_dirty = false) {
+    if (allow_dirty && eng.fresh[kind]) {
+      eng.pre(kProfDetectDirty);
+      k_detect_dirty<<<blocks(n() / 16 + 1, 16), 256, 0, ws.stream>>>(s().fdir, s().gdir, n(), s().cstamp,
+                                                                      eng.end_mark[kind], kind, list, count,
+                                                                      act_lo, act_hi);
+      eng.launched(kProfDetectDirty);
+    } else {
+      eng.pre(kProfDetectKind);
+      k_detect_range<<<blocks((act_hi - act_lo) / 16 + 1, 16), 256, 0, ws.stream>>>(
+          s().fdir, s().gdir, act_lo, act_hi, kind, list, count);
+      eng.launched(kProfDetectKind);
+    }
     ++st().detect_sweeps;
   }
 
@@ -762,7 +772,7 @@ struct SlabEngine {
     State<T>& S = s();
     uint32_t& cur = eng.cur;
     reset_ctl();
-    detect(kind, S.list[cur], &ws.ctl->list_count[cur]);
+    detect(kind, S.list[cur], &ws.ctl->list_count[cur], /*allow_dirty=*/true);
     const uint32_t batch_base = ws.next_batch, mark_base = ws.next_mark;
     uint64_t attempted = 0, iters = 0, edits = 0;
     struct IdGuard {
@@ -839,7 +849,11 @@ struct SlabEngine {
     for (;;) {
       ++st().c_passes;
       uint64_t pass_edits = 0;
-      for (int kind = 0; kind < 4; ++kind) pass_edits += run_subloop(kind);
+      for (int kind = 0; kind < 4; ++kind) {
+        pass_edits += run_subloop(kind);
+        eng.end_mark[kind] = ws.next_mark;  // every later batch uses marks >= this
+        eng.fresh[kind] = true;
+      }
       if (pass_edits == 0) return;
     }
   }
