@@ -331,6 +331,7 @@ struct Engine {
   uint32_t end_mark[4] = {0, 0, 0, 0};
   bool fresh[4] = {false, false, false, false};
   float dir_ms = 0.f, lab_ms = 0.f;
+  SlabRes sres{};  // z-slab label resolution for k_rfix_tiles (tab == nullptr: single device)
 
   const T* fhat = nullptr;  // decompressed input on the device (derives touched at compaction)
 
@@ -487,6 +488,8 @@ struct Engine {
     t.affected = ws.taffected.as<uint8_t>();
     t.mis_bits = ws.tbits.as<uint32_t>();
     t.mis_cnt = ws.tcnt.as<uint32_t>();
+    t.own_lo = s.own_n ? s.own_lo : 0u;
+    t.own_hi = s.own_n ? s.own_lo + s.own_n : n();
     return t;
   }
   uint32_t* tile_list(int k) const { return ws.tlist.as<uint32_t>() + size_t(k) * label_tiles(); }
@@ -584,7 +587,8 @@ struct Engine {
 
   // R batch targets from the tile mismatch bitmaps (k_rfix_tiles on the given
   // tiles first); returns the total mismatch count, targets in list(0).
-  uint64_t r_targets(bool all_tiles) {
+  // raise_trouble = false (z-slab ranks): the status word is all-gathered instead
+  uint64_t r_targets(bool all_tiles, bool raise_trouble = true) {
     TileStore ts = tile_store();
     uint32_t nt = ts.ntiles;
     const uint32_t* list = nullptr;
@@ -597,9 +601,9 @@ struct Engine {
     if (nt) {
       pre(kProfRfix);
       if (geo.ndims == 2)
-        k_rfix_tiles<T, 2><<<nt, 256, 0, ws.stream>>>(s, list, ts, fin(0), fin(1));
+        k_rfix_tiles<T, 2><<<nt, 256, 0, ws.stream>>>(s, list, ts, fin(0), fin(1), sres);
       else
-        k_rfix_tiles<T, 3><<<nt, 256, 0, ws.stream>>>(s, list, ts, fin(0), fin(1));
+        k_rfix_tiles<T, 3><<<nt, 256, 0, ws.stream>>>(s, list, ts, fin(0), fin(1), sres);
       launched(kProfRfix);
     }
     st.rfix_tiles += nt;
@@ -616,7 +620,7 @@ struct Engine {
     }
     CK(cudaMemsetAsync(ts.dirty, 0, ts.ntiles, ws.stream));
     ws.pull_ctl();
-    if (ws.hctl->status == kStatusTroubleMax)
+    if (raise_trouble && ws.hctl->status == kStatusTroubleMax)
       fail(MSSZ_CU_ERR_INTERNAL, "troublemaker target is an extremum (stale critical report)");
     return ws.hctl->mism;
   }

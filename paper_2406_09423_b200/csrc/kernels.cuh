@@ -72,6 +72,55 @@ __device__ __forceinline__ uint32_t label_tile_of(const Geom& g, uint32_t x, uin
   return x / TL::TX + ntx * (y / TL::TY + nty * (DIM == 2 ? 0u : z / TL::TZ));
 }
 
+// z-slab partition for label-table lookups on the device (shard.cuh)
+constexpr int kMaxSlabs = 64;
+
+struct SlabTable {  // the z partition, for label-table lookups on the device
+  uint32_t P, XY;
+  uint32_t z0[kMaxSlabs + 1];  // z0[P] = Z
+};
+
+__device__ __forceinline__ int slab_owner(const SlabTable& t, uint32_t z) {
+  int lo = 0, hi = static_cast<int>(t.P) - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (t.z0[mid] <= z) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// Slot of global vertex L in the gathered label table [rank][family][side][xy],
+// or -1 when L is not on the first (side 0) or last (side 1) plane of its slab.
+__device__ __forceinline__ int64_t table_slot(const SlabTable& t, uint32_t L, int fam) {
+  const uint32_t z = L / t.XY;
+  const int r = slab_owner(t, z);
+  int side;
+  if (z == t.z0[r]) side = 0;
+  else if (z + 1 == t.z0[r + 1]) side = 1;
+  else return -1;
+  return ((static_cast<int64_t>(r) * 2 + fam) * 2 + side) * t.XY + (L - z * t.XY);
+}
+
+// R target slot a rank does not own (z-slab windows): fix_batch's ownership test
+// rejects it (ids are < 2^32 - 1)
+constexpr uint32_t kNoTarget = 0xFFFFFFFFu;
+
+// z-slab label resolution for the tile-based R kernels: a window-local final
+// label lying on a slab boundary plane is replaced by its resolved table entry.
+// tab == nullptr on a single device (labels are already final).
+struct SlabRes {
+  const uint32_t* tab;
+  SlabTable t;
+  uint32_t base;  // global id of window vertex 0
+};
+__device__ __forceinline__ uint32_t resolve_label(const SlabRes& r, uint32_t local, int fam) {
+  if (!r.tab) return local;
+  const uint32_t L = local + r.base;
+  const int64_t sl = table_slot(r.t, L, fam);
+  return sl >= 0 ? __ldg(r.tab + sl) : L;
+}
+
 template <class T>
 struct State;
 
@@ -1238,6 +1287,9 @@ struct TileStore {
   uint32_t* mis_cnt;  // [ntiles]
   uint32_t ntiles;
   uint32_t surface;   // LabelTile<DIM>::kSurface
+  // vertices outside [own_lo, own_hi) are labelled as extrema (z-slab windows:
+  // chains stop at their first off-slab vertex); single device: the whole grid
+  uint32_t own_lo, own_hi;
 };
 
 // Phase 1.  Writes the provisional label (root, or first vertex outside the
@@ -1305,15 +1357,19 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
     for (int q = threadIdx.x; q < kLabelTileN / 16; q += kLabelTileThreads) {
       const int row = q / VPR, c = q % VPR;
       const int ly = row & (TL::TY - 1), lz = row / TL::TY;
-      const uint4 w = __ldg(reinterpret_cast<const uint4*>(dir + base + g.X * ly + g.XY * lz) + c);
+      const uint32_t gv = base + g.X * ly + g.XY * lz + 16 * c;  // own bounds are plane (16 B) aligned here
+      const uint4 w = (gv >= ts.own_lo && gv < ts.own_hi)
+                          ? __ldg(reinterpret_cast<const uint4*>(dir + base + g.X * ly + g.XY * lz) + c)
+                          : make_uint4(~0u, ~0u, ~0u, ~0u);
       reinterpret_cast<uint4*>(sdir)[q] = w;
     }
   } else {
 #pragma unroll 4
     for (int i = threadIdx.x; i < kLabelTileN; i += kLabelTileThreads) {
       const int lx = i & (TL::TX - 1), ly = (i >> TL::LX) & (TL::TY - 1), lz = i >> (TL::LX + TL::LY);
-      const bool val = lx < ex && ly < ey && lz < ez;
-      sdir[i] = val ? __ldg(dir + base + lx + g.X * ly + g.XY * lz) : 0xFF;
+      const uint32_t gv = base + lx + g.X * ly + g.XY * lz;
+      const bool val = lx < ex && ly < ey && lz < ez && gv >= ts.own_lo && gv < ts.own_hi;
+      sdir[i] = val ? __ldg(dir + gv) : 0xFF;
     }
   }
   __syncthreads();
@@ -1623,7 +1679,7 @@ __global__ void k_u32_to_u64(const uint32_t* __restrict__ in, uint64_t* __restri
 template <class T, int DIM>
 __global__ void __launch_bounds__(256) k_rfix_tiles(State<T> s, const uint32_t* __restrict__ tiles,
                                                     TileStore ts, const uint32_t* __restrict__ finM,
-                                                    const uint32_t* __restrict__ finm) {
+                                                    const uint32_t* __restrict__ finm, SlabRes sr) {
   using TL = LabelTile<DIM>;
   const Geom& g = s.geo;
   const uint32_t ntx = (g.X + TL::TX - 1) / TL::TX;
@@ -1640,8 +1696,8 @@ __global__ void __launch_bounds__(256) k_rfix_tiles(State<T> s, const uint32_t* 
   for (int i = threadIdx.x; i < kLabelTileN; i += blockDim.x) {
     const int lx = i & (TL::TX - 1), ly = (i >> TL::LX) & (TL::TY - 1), lz = i >> (TL::LX + TL::LY);
     bool ma = false, md = false;
-    if (lx < ex && ly < ey && lz < ez) {
-      const uint32_t v = base + lx + g.X * ly + g.XY * lz;
+    const uint32_t v = base + lx + g.X * ly + g.XY * lz;
+    if (lx < ex && ly < ey && lz < ez && v - s.act_lo < s.act_n) {
       const uint32_t fc = __ldg(s.fdir + v), gc = __ldg(s.gdir + v);
       const bool wa = (gc & 15u) != (fc & 15u);  // ascending line diverges at v
       const bool wd = (gc >> 4) != (fc >> 4);    // descending line diverges at v
@@ -1654,8 +1710,8 @@ __global__ void __launch_bounds__(256) k_rfix_tiles(State<T> s, const uint32_t* 
         ld = __ldg(s.gm + v);
         fd = __ldg(s.fm + v);
       }
-      ma = wa && __ldg(finM + la) != fa;
-      md = wd && __ldg(finm + ld) != fd;
+      ma = wa && resolve_label(sr, __ldg(finM + la), 0) != fa;
+      md = wd && resolve_label(sr, __ldg(finm + ld), 1) != fd;
     }
     const uint32_t wa_bits = __ballot_sync(0xffffffffu, ma);
     const uint32_t wd_bits = __ballot_sync(0xffffffffu, md);
@@ -1703,8 +1759,12 @@ __global__ void __launch_bounds__(256) k_expand_targets(State<T> s, const uint32
       const int lx = i & (TL::TX - 1), ly = (i >> TL::LX) & (TL::TY - 1), lz = i >> (TL::LX + TL::LY);
       const uint32_t v = base + lx + g.X * ly + g.XY * lz;
       const uint32_t code = fam ? (__ldg(s.fdir + v) >> 4) : (__ldg(s.gdir + v) & 15u);
-      if (code == kSelf) atomicExch(&s.ctl->status, kStatusTroubleMax);
-      targets[pos++] = code == kSelf ? v : v + g.off[code];
+      const bool owned = v - s.own_lo < s.own_n;
+      if (code == kSelf && owned) atomicExch(&s.ctl->status, kStatusTroubleMax);
+      const uint32_t t = code == kSelf ? v : v + g.off[code];
+      // owner-computes (z-slab windows): only targets this rank owns; on a
+      // single device every target is owned.  A dropped slot keeps the list dense.
+      targets[pos++] = t - s.own_lo < s.own_n ? t : kNoTarget;
     }
   }
 #pragma unroll

@@ -26,7 +26,9 @@
 // all-gather the provisional labels of their first and last owned planes and
 // resolve every table entry to its chain terminus by pointer chasing on the
 // gathered table; a vertex's final label is then its provisional label, or
-// that label's table entry when the label lies on a boundary plane.
+// that label's table entry when the label lies on a boundary plane.  The R loop
+// is incremental as on a single device (dirty label tiles, tile mismatch bits),
+// plus tiles whose labels depend on a boundary-table entry that changed.
 //
 // Transports: NCCL (one process per GPU; ncclAllGather for the per-batch
 // status records and the label tables, grouped ncclSend/ncclRecv with the z
@@ -44,41 +46,12 @@
 namespace mssz_b200 {
 namespace {
 
-constexpr int kMaxSlabs = 64;
-
 // (global id, lowered value) of a boundary target.
 template <class T>
 struct BEdit {
   uint32_t idx;
   T val;
 };
-
-struct SlabTable {  // the z partition, for label-table lookups on the device
-  uint32_t P, XY;
-  uint32_t z0[kMaxSlabs + 1];  // z0[P] = Z
-};
-
-__device__ __forceinline__ int slab_owner(const SlabTable& t, uint32_t z) {
-  int lo = 0, hi = static_cast<int>(t.P) - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (t.z0[mid] <= z) lo = mid;
-    else hi = mid - 1;
-  }
-  return lo;
-}
-
-// Slot of global vertex L in the gathered label table [rank][family][side][xy],
-// or -1 when L is not on the first (side 0) or last (side 1) plane of its slab.
-__device__ __forceinline__ int64_t table_slot(const SlabTable& t, uint32_t L, int fam) {
-  const uint32_t z = L / t.XY;
-  const int r = slab_owner(t, z);
-  int side;
-  if (z == t.z0[r]) side = 0;
-  else if (z + 1 == t.z0[r + 1]) side = 1;
-  else return -1;
-  return ((static_cast<int64_t>(r) * 2 + fam) * 2 + side) * t.XY + (L - z * t.XY);
-}
 
 // Per-batch status record, all-gathered across ranks.
 struct alignas(8) Rec {
@@ -94,7 +67,8 @@ struct alignas(8) Rec {
   uint64_t err;       // label-table resolution hit a cycle
 };
 
-__global__ void k_rec(const Ctl* __restrict__ ctl, uint32_t cur, Rec* __restrict__ out) {
+__global__ void k_rec(const Ctl* __restrict__ ctl, uint32_t cur, const uint32_t* __restrict__ err,
+                      Rec* __restrict__ out) {
   if (threadIdx.x != 0) return;
   Rec r;
   r.list = ctl->list_count[cur];
@@ -106,7 +80,7 @@ __global__ void k_rec(const Ctl* __restrict__ ctl, uint32_t cur, Rec* __restrict
   r.status = ctl->status;
   r.nonfinite = ctl->nonfinite;
   r.violations = ctl->violations;
-  r.err = ctl->sp_abort;
+  r.err = *err;
   *out = r;
 }
 
@@ -259,26 +233,6 @@ __global__ void __launch_bounds__(256) k_count_false_range(const uint8_t* __rest
     atomicAdd(reinterpret_cast<unsigned long long*>(total), static_cast<unsigned long long>(c));
 }
 
-// Label input for one slab: the window's direction codes with every non-owned
-// vertex turned into an extremum (SELF both ways), so chains stop at the first
-// vertex outside [own_lo, own_hi).
-__global__ void __launch_bounds__(256) k_mask_dir(const uint8_t* __restrict__ dir, uint32_t n,
-                                                  uint32_t own_lo, uint32_t own_hi,
-                                                  uint8_t* __restrict__ out) {
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q * 16 < n; q += stride) {
-    const uint64_t v0 = q * 16;
-    if (v0 >= own_lo && v0 + 16 <= own_hi && v0 + 16 <= n) {
-      reinterpret_cast<uint4*>(out)[q] = __ldg(reinterpret_cast<const uint4*>(dir) + q);
-    } else {
-      for (int j = 0; j < 16 && v0 + j < n; ++j) {
-        const uint64_t v = v0 + j;
-        out[v] = (v >= own_lo && v < own_hi) ? dir[v] : uint8_t(0xFF);
-      }
-    }
-  }
-}
-
 // Window labels of the first / last owned plane -> this rank's table part
 // [family][side][xy] (global ids).  Label = fin[prov[v]] (label_pass without
 // its finish phase: prov is a root or a resolved exit).
@@ -351,67 +305,59 @@ __global__ void __launch_bounds__(256) k_final_labels(const uint32_t* __restrict
   }
 }
 
-// Final global g label of a window vertex from its provisional label.
-__device__ __forceinline__ uint32_t g_final(const uint32_t* __restrict__ prov, const uint32_t* __restrict__ fin,
-                                            const uint32_t* __restrict__ tab, const SlabTable& t,
-                                            uint32_t base, int resolve, uint32_t v, int fam) {
-  uint32_t L = __ldg(fin + __ldg(prov + v)) + base;
-  if (resolve) {
-    const int64_t sl = table_slot(t, L, fam);
-    if (sl >= 0) L = __ldg(tab + sl);
+// Boundary-table entries that changed since the previous R iteration (the
+// resolved table is then kept as the reference for the next one).
+__global__ void __launch_bounds__(256) k_table_diff(const uint32_t* __restrict__ tab, uint32_t* __restrict__ prev,
+                                                    uint8_t* __restrict__ changed, uint64_t total,
+                                                    uint32_t* any) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  bool c_any = false;
+  for (uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const uint32_t a = tab[e];
+    const bool c = a != prev[e];
+    changed[e] = c ? 1 : 0;
+    if (c) {
+      prev[e] = a;
+      c_any = true;
+    }
   }
-  return L;
+  if (__any_sync(0xffffffffu, c_any) && (threadIdx.x & 31) == 0) *any = 1u;
 }
 
-// R batch targets over the active range (see k_rfix_tiles for the walk-free
-// argument; find_troublemaker, edit_engine.cpp:293-315): a divergent vertex w
-// whose final label differs contributes g-asc(w) / f-desc(w).  Targets are
-// kept by their owner only; mismatches are counted on owned vertices only.
-// g labels are resolved only for divergent vertices (no full finish pass).
-template <class T>
-__global__ void __launch_bounds__(256) k_slab_rtargets(State<T> s, const uint32_t* __restrict__ gM,
-                                                       const uint32_t* __restrict__ gm,
-                                                       const uint32_t* __restrict__ finM,
+// Tiles whose final labels depend on changed table entries become "affected":
+// tiles holding non-owned window planes (their vertices' labels are table
+// entries or chains into them), and tiles with an exit whose final label is an
+// off-slab vertex on a changed entry.  CTA per tile.
+template <int DIM>
+__global__ void __launch_bounds__(256) k_slab_affected(TileStore ts, const uint32_t* __restrict__ finM,
                                                        const uint32_t* __restrict__ finm,
-                                                       const uint32_t* __restrict__ tab, SlabTable tb,
-                                                       uint32_t base, int resolve,
-                                                       uint32_t* __restrict__ targets, uint32_t* count) {
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  const uint64_t hi = static_cast<uint64_t>(s.act_lo) + s.act_n;
-  uint32_t mism = 0;
-  for (uint64_t wb = s.act_lo + ((static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) & ~uint64_t(31));
-       wb < hi; wb += stride) {
-    const uint64_t v = wb + (threadIdx.x & 31);
-    bool ta = false, td = false;
-    uint32_t xa = 0, xd = 0;
-    if (v < hi) {
-      const uint32_t fc = __ldg(s.fdir + v), gc = __ldg(s.gdir + v);
-      const bool owned = v - s.own_lo < s.own_n;
-      const bool ma = (gc & 15u) != (fc & 15u) &&
-                      g_final(gM, finM, tab, tb, base, resolve, v, 0) != __ldg(s.fM + v);
-      const bool md = (gc >> 4) != (fc >> 4) &&
-                      g_final(gm, finm, tab, tb, base, resolve, v, 1) != __ldg(s.fm + v);
-      if (owned) mism += (ma ? 1u : 0u) + (md ? 1u : 0u);
-      if (ma) {
-        const uint32_t c = gc & 15u;
-        if (c == kSelf && owned) atomicExch(&s.ctl->status, kStatusTroubleMax);
-        xa = c == kSelf ? static_cast<uint32_t>(v) : static_cast<uint32_t>(v) + s.geo.off[c];
-        ta = xa - s.own_lo < s.own_n;
-      }
-      if (md) {
-        const uint32_t c = fc >> 4;
-        if (c == kSelf && owned) atomicExch(&s.ctl->status, kStatusTroubleMax);
-        xd = c == kSelf ? static_cast<uint32_t>(v) : static_cast<uint32_t>(v) + s.geo.off[c];
-        td = xd - s.own_lo < s.own_n;
+                                                       const uint8_t* __restrict__ changed, const uint32_t* any,
+                                                       SlabTable t, Geom g, uint32_t base) {
+  using TL = LabelTile<DIM>;
+  if (!*any) return;
+  const uint32_t b = blockIdx.x;
+  const uint32_t ntx = (g.X + TL::TX - 1) / TL::TX, nty = (g.Y + TL::TY - 1) / TL::TY;
+  const uint32_t tz = b / (ntx * nty);
+  const uint64_t zlo = static_cast<uint64_t>(tz) * TL::TZ, zhi = min(zlo + TL::TZ, static_cast<uint64_t>(g.Z));
+  if (zlo * g.XY < ts.own_lo || zhi * g.XY > ts.own_hi) {
+    if (threadIdx.x == 0) ts.affected[b] = 1;
+    return;
+  }
+  bool hit = false;
+#pragma unroll
+  for (int fam = 0; fam < 2; ++fam) {
+    const uint32_t* E = ts.E + (static_cast<size_t>(b) * 2 + fam) * ts.surface;
+    const uint32_t ne = ts.Ecnt[b * 2 + fam];
+    const uint32_t* fin = fam ? finm : finM;
+    for (uint32_t k = threadIdx.x; k < ne; k += blockDim.x) {
+      const uint32_t L = fin[E[k]];
+      if (L < ts.own_lo || L >= ts.own_hi) {
+        const int64_t sl = table_slot(t, L + base, fam);
+        hit |= sl >= 0 && changed[sl];
       }
     }
-    warp_append(ta, xa, targets, count);
-    warp_append(td, xd, targets, count);
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mism += __shfl_xor_sync(0xffffffffu, mism, o);
-  if ((threadIdx.x & 31) == 0 && mism)
-    atomicAdd(reinterpret_cast<unsigned long long*>(&s.ctl->mism), static_cast<unsigned long long>(mism));
+  if (__syncthreads_or(hit) && threadIdx.x == 0) ts.affected[b] = 1;
 }
 
 // ---------------------------------------------------------------------------
@@ -618,10 +564,11 @@ SlabPlan slab_plan(uint64_t Z, int P, int r) {
 
 // Workspace extras of the sharded loop.
 struct SlabBufs {
-  DevBuf ldir, tab_mine, tab_all, send[2], recv[2], rec, rec_all;
+  DevBuf tab_mine, tab_all, tab_prev, tchanged, send[2], recv[2], rec, rec_all;
+  DevBuf flags;  // [0] table resolution hit a cycle, [1] a table entry changed
   std::vector<Rec> hrec;
   void release() {
-    for (DevBuf* b : {&ldir, &tab_mine, &tab_all, &send[0], &send[1], &recv[0], &recv[1], &rec, &rec_all})
+    for (DevBuf* b : {&tab_mine, &tab_all, &tab_prev, &tchanged, &flags, &send[0], &send[1], &recv[0], &recv[1], &rec, &rec_all})
       b->release();
   }
 };
@@ -653,14 +600,16 @@ struct SlabEngine {
     stab.XY = XY;
     for (uint32_t r = 0; r <= pl.P; ++r) stab.z0[r] = static_cast<uint32_t>(uint64_t(pl.Z) * r / pl.P);
     const size_t nw = eng.n();
-    sb.ldir.ensure(nw + 16);
     sb.tab_mine.ensure(size_t(4) * XY * 4);
     sb.tab_all.ensure(size_t(4) * XY * 4 * pl.P);
+    sb.tab_prev.ensure(size_t(4) * XY * 4 * pl.P);
+    sb.tchanged.ensure(size_t(4) * XY * pl.P);
     for (int k = 0; k < 2; ++k) {
       sb.send[k].ensure(size_t(2) * XY * sizeof(BEdit<T>));
       sb.recv[k].ensure(size_t(2) * XY * sizeof(BEdit<T>));
     }
     sb.rec.ensure(sizeof(Rec));
+    sb.flags.ensure(16);
     sb.rec_all.ensure(sizeof(Rec) * pl.P);
     sb.hrec.resize(pl.P);
   }
@@ -672,7 +621,7 @@ struct SlabEngine {
 
   // all-gathered status records of every rank (blocking)
   const std::vector<Rec>& gather() {
-    k_rec<<<1, 32, 0, ws.stream>>>(ws.ctl, eng.cur, sb.rec.as<Rec>());
+    k_rec<<<1, 32, 0, ws.stream>>>(ws.ctl, eng.cur, sb.flags.as<uint32_t>(), sb.rec.as<Rec>());
     CK_LAUNCH();
     tr.allgather_status(sb.rec.p, sb.rec_all.p, sb.hrec.data(), sizeof(Rec), ws.stream);
     return sb.hrec;
@@ -736,16 +685,15 @@ struct SlabEngine {
   }
 
   // ---- labels of one direction field (f at setup, g per R iteration) ----
-  // Window labels with the off-slab vertices masked as extrema, then the
-  // boundary tables.  finals: also write final global labels of the active
-  // range to FM / Fm (f); otherwise (g) k_slab_rtargets resolves them lazily.
-  void labels(const uint8_t* dir, uint32_t* FM, uint32_t* Fm, bool finals) {
-    eng.pre(kProfLabelInit);
-    k_mask_dir<<<blocks(n() / 16 + 1, 16), 256, 0, ws.stream>>>(dir, n(), own_lo, own_hi, sb.ldir.as<uint8_t>());
-    eng.launched(kProfLabelInit);
+  // Window labels with the off-slab vertices masked as extrema (TileStore own
+  // range), then the boundary tables.  finals: also write final global labels of
+  // the active range to FM / Fm (f); g labels are resolved per tile by
+  // k_rfix_tiles through SlabRes.
+  void labels(const uint8_t* dir, uint32_t* FM, uint32_t* Fm, bool finals, bool only_dirty = false) {
     uint32_t* M = eng.lab(2);
     uint32_t* m = eng.lab(3);
-    eng.label_pass(sb.ldir.as<uint8_t>(), M, m, /*only_dirty=*/false, /*finish=*/false);
+    // the tile store masks vertices outside [own_lo, own_hi) as extrema
+    eng.label_pass(dir, M, m, only_dirty, /*finish=*/false);
     const bool multi = pl.P > 1;
     if (multi) {
       eng.pre(kProfLabelJump);
@@ -753,10 +701,9 @@ struct SlabEngine {
                                                                   own_hi, base, sb.tab_mine.as<uint32_t>());
       eng.launched(kProfLabelJump);
       tr.allgather_dev(sb.tab_mine.p, sb.tab_all.p, size_t(4) * XY * 4, ws.stream);
-      CK(cudaMemsetAsync(&ws.ctl->sp_abort, 0, 4, ws.stream));
       eng.pre(kProfLabelJump);
       k_resolve_table<<<blocks(4ull * XY * pl.P, 16), 256, 0, ws.stream>>>(sb.tab_all.as<uint32_t>(), stab,
-                                                                            &ws.ctl->sp_abort);
+                                                                            sb.flags.as<uint32_t>());
       eng.launched(kProfLabelJump);
     }
     if (!finals) return;
@@ -854,6 +801,7 @@ struct SlabEngine {
         eng.end_mark[kind] = ws.next_mark;  // every later batch uses marks >= this
         eng.fresh[kind] = true;
       }
+      if (pass_edits) r_full_valid = false;  // the C loop does not track dirty label tiles
       if (pass_edits == 0) return;
     }
   }
@@ -872,17 +820,38 @@ struct SlabEngine {
   }
 
   // g labels + R targets + (speculative) fix; returns the global mismatch count
+  // Incremental R batch, as on a single device (Engine::run_r_loop): after a
+  // full pass only label tiles whose codes changed are re-resolved, and only
+  // tiles that are dirty or whose exits' finals changed recompute their
+  // mismatch bits -- plus, across slabs, tiles whose labels depend on a
+  // boundary-table entry that changed (k_slab_affected).
+  bool r_full_valid = false;
   uint64_t r_batch(uint32_t batch) {
-    labels(s().gdir, nullptr, nullptr, false);
-    // label_pass used list_count[0] as a scratch counter
-    CK(cudaMemsetAsync(&ws.ctl->list_count[0], 0, sizeof(uint32_t), ws.stream));
-    CK(cudaMemsetAsync(&ws.ctl->mism, 0, sizeof(uint64_t), ws.stream));
-    CK(cudaMemsetAsync(&ws.ctl->status, 0, sizeof(uint32_t), ws.stream));
-    eng.pre(kProfRfix);
-    k_slab_rtargets<T><<<blocks(act_hi - act_lo, 16), 256, 0, ws.stream>>>(
-        s(), eng.lab(2), eng.lab(3), eng.fin(0), eng.fin(1), sb.tab_all.as<uint32_t>(), stab, base,
-        pl.P > 1 ? 1 : 0, eng.list(0), &ws.ctl->list_count[0]);
-    eng.launched(kProfRfix);
+    const bool incr = r_full_valid;
+    TileStore ts = eng.tile_store();
+    CK(cudaMemsetAsync(sb.flags.p, 0, 8, ws.stream));
+    labels(s().gdir, nullptr, nullptr, false, incr);
+    if (pl.P > 1) {
+      const uint64_t tot = 4ull * XY * pl.P;
+      if (incr) {
+        eng.pre(kProfLabelJump);
+        k_table_diff<<<blocks(tot, 16), 256, 0, ws.stream>>>(sb.tab_all.as<uint32_t>(), sb.tab_prev.as<uint32_t>(),
+                                                            sb.tchanged.as<uint8_t>(), tot,
+                                                            sb.flags.as<uint32_t>() + 1);
+        eng.launched(kProfLabelJump);
+        eng.pre(kProfLabelJump);
+        k_slab_affected<3><<<ts.ntiles, 256, 0, ws.stream>>>(ts, eng.fin(0), eng.fin(1), sb.tchanged.as<uint8_t>(),
+                                                            sb.flags.as<uint32_t>() + 1, stab, eng.geo, base);
+        eng.launched(kProfLabelJump);
+      } else {
+        CK(cudaMemcpyAsync(sb.tab_prev.p, sb.tab_all.p, tot * 4, cudaMemcpyDeviceToDevice, ws.stream));
+      }
+      eng.sres = SlabRes{sb.tab_all.as<uint32_t>(), stab, base};
+    } else {
+      eng.sres = SlabRes{nullptr, stab, base};  // one slab: window labels are final
+    }
+    eng.r_targets(/*all_tiles=*/!incr, /*raise_trouble=*/false);  // targets -> list(0), ctl->mism / status
+    r_full_valid = true;
     fix(0, batch, eng.list(0), &ws.ctl->list_count[0], false);
     gather();
     if (sum([](const Rec& r) { return r.err; }))
@@ -896,6 +865,12 @@ struct SlabEngine {
   bool run_r_loop() {
     uint64_t iters = 0;
     bool first = true, last_frontier = false;
+    TileStore ts = eng.tile_store();
+    struct DirtyOff {
+      State<T>& s;
+      ~DirtyOff() { s.tdirty = nullptr; }
+    } dirty_off{s()};
+    s().tdirty = ts.dirty;  // the R-loop frontier marks the label tiles it changes
     for (;;) {
       if (!first && count_false(last_frontier) != 0) return false;
       first = false;
@@ -911,6 +886,7 @@ struct SlabEngine {
       CK(cudaMemsetAsync(&ws.ctl->f_count, 0, sizeof(uint32_t), ws.stream));
       if (applied > n_glob / kRHugeDivisor) {
         eng.directions(s().g, s().gdir);
+        CK(cudaMemsetAsync(ts.dirty, 1, ts.ntiles, ws.stream));  // every tile may have changed
         last_frontier = false;
       } else {
         last_frontier = true;
@@ -952,6 +928,8 @@ struct SlabEngine {
     st().input_bound_violations = violations;
 
     CK(cudaMemsetAsync(S.touched, 0, n(), ws.stream));
+    CK(cudaMemsetAsync(sb.flags.p, 0, 16, ws.stream));
+    r_full_valid = false;
     CK(cudaEventRecord(ws.ev[0], ws.stream));
     eng.directions(d_f, ws.fdir.as<uint8_t>());
     eng.directions(S.g, S.gdir);
