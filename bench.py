@@ -421,6 +421,20 @@ def main():
                       "api": "mssz_cu_compress_base / mssz_cu_decompress_base (block wavefront)"}
         del recon, sym, lits, back
 
+    # ---- edit-set encoding of this EditSet, store backend:
+    # the GPU stages (delta, LEB128, RLE, histogram, bit packing) are timed
+    edit_codec = None
+    if not sharded:
+        es_host = P.EditSet(d_idx[:count].cpu().numpy().astype(np.uint64), d_val[:count].cpu().numpy())
+        tm = {}
+        t0 = time.perf_counter()
+        payload = P.encode_edits(es_host, 0, tm)
+        wall = time.perf_counter() - t0
+        edit_codec = {"edits": int(count), "payload_bytes": len(payload), "device_ms": tm["device_ms"],
+                      "wall_ms": wall * 1e3, "codec": "store",
+                      "api": "mssz_cu_encode_edits (byte-identical to encode_edits, edit_codec.cpp:188-222)"}
+        del es_host, payload
+
     # ---- e2e through the host API with pinned buffers
     e2e = None
     if not args.no_e2e:
@@ -492,6 +506,7 @@ def main():
         "e2e": e2e,
         "verify": verify,
         "base_codec": base_codec,
+        "edit_codec": edit_codec,
         "gpu_launches": int(dist.sum(float(sum(s.kernel_launches for s in stats)))),
         "clocks": clk,
         "edit_stats": {"outer_iterations": st.outer_iterations, "c_passes": st.c_passes,

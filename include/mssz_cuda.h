@@ -281,6 +281,18 @@ int mssz_cu_decompress_base_f32(int ndims, const uint64_t* dims, const uint32_t*
 int mssz_cu_decompress_base_f64(int ndims, const uint64_t* dims, const uint32_t* symbols, const double* literals,
                                 uint64_t n_literals, double xi, double* recon, double* device_ms);
 
+/* ---- edit-set encoding: encode_edits<T>, edit_codec.cpp:188-222 ----
+ * Byte-identical payload: u64 count, u64 index-stream length, index stream =
+ * backend(huffman(rle(leb128(delta(indices))))), value stream = backend(raw LE
+ * values); codec 0 = store, 1 = raw DEFLATE (zlib, as the reference).  Delta,
+ * LEB128, RLE, the histogram and the bit packing run on the GPU; code lengths
+ * and DEFLATE on the host.  Payload is callee-allocated (mssz_cu_free);
+ * device_ms (nullable) = device time of the GPU stages. */
+int mssz_cu_encode_edits_f32(const uint64_t* indices, const float* values, uint64_t count, int codec,
+                             uint8_t** payload, uint64_t* payload_len, double* device_ms);
+int mssz_cu_encode_edits_f64(const uint64_t* indices, const double* values, uint64_t count, int codec,
+                             uint8_t** payload, uint64_t* payload_len, double* device_ms);
+
 #ifdef __cplusplus
 }
 #endif

@@ -259,6 +259,18 @@ class Ref(_Lib):
             max_steps, _ptr(trace), C.byref(steps), _ptr(floor)))
         return trace[: steps.value + 1], floor[0]
 
+    def encode_edits(self, indices: np.ndarray, values: np.ndarray, codec: int = 1) -> bytes:
+        """encode_edits<T> (edit_codec.cpp:188-222): the reference edit payload."""
+        idx = np.ascontiguousarray(indices, np.uint64)
+        val = np.ascontiguousarray(values)
+        out = C.POINTER(C.c_uint8)()
+        n = C.c_uint64()
+        self._check(self._fn(f"encode_edits_{_suffix(val.dtype)}")(
+            _ptr(idx), _ptr(val), C.c_uint64(idx.size), codec, C.byref(out), C.byref(n)))
+        data = bytes(C.cast(out, C.POINTER(C.c_uint8 * max(n.value, 1))).contents)[:n.value]
+        self.lib.mssz_ref_free(C.cast(out, C.c_void_p))
+        return data
+
     def find_troublemaker(self, dims, f, g, xi, v, descending=False):
         vi = C.c_uint64()
         vt = C.c_uint64()

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "mssz/base_codec.hpp"
+#include "mssz/edit_codec.hpp"
 #include "mssz/edit_engine.hpp"
 #include "mssz/field.hpp"
 #include "mssz/grid.hpp"
@@ -300,6 +301,23 @@ int mssz_ref_compute_labels(int ndims, const uint64_t* dims, const uint64_t* asc
     std::memcpy(m, l.min_label.data(), sizeof(uint64_t) * topo.vertex_count);
   });
 }
+
+// encode_edits<T> (edit_codec.cpp:188-222): callee-allocated payload (mssz_ref_free)
+#define MSSZ_REF_CODEC(SUF, T)                                                                 \
+  int mssz_ref_encode_edits_##SUF(const uint64_t* idx, const T* val, uint64_t count, int codec, \
+                                  uint8_t** out, uint64_t* len) {                               \
+    return guarded([&] {                                                                        \
+      EditSet<T> e;                                                                             \
+      e.indices.assign(idx, idx + count);                                                       \
+      e.values.assign(val, val + count);                                                        \
+      const auto bytes = encode_edits<T>(e, parse_backend(static_cast<std::uint8_t>(codec)));   \
+      *out = static_cast<uint8_t*>(std::malloc(bytes.size() ? bytes.size() : 1));               \
+      std::memcpy(*out, bytes.data(), bytes.size());                                            \
+      *len = bytes.size();                                                                      \
+    });                                                                                         \
+  }
+MSSZ_REF_CODEC(f32, float)
+MSSZ_REF_CODEC(f64, double)
 
 int mssz_ref_build_topology(int ndims, const uint64_t* dims, uint64_t* vertex_count) {
   return guarded([&] { *vertex_count = topo_of(ndims, dims).vertex_count; });

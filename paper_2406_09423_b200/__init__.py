@@ -34,7 +34,7 @@ __all__ = [
     "detect_kind", "lower_step", "representable_floor", "apply_edits", "segmentation_equal",
     "library", "build", "slab_range", "derive_edits_slabs", "SlabComm",
     "VerificationReport", "build_report", "build_report_device", "segmentation", "export_labels",
-    "compress_base", "decompress_base",
+    "compress_base", "decompress_base", "encode_edits",
 ]
 
 FPMAX, FPMIN, FNMAX, FNMIN = 0, 1, 2, 3
@@ -281,7 +281,7 @@ EXPORTS = [
         "compute_direction_codes", "detect_false_critical", "detect_kind", "lower_step",
         "representable_floor", "apply_edits", "derive_edits_slab", "derive_edits_slab_device",
         "derive_edits_slabs_local", "verify", "verify_device", "segmentation", "compress_base",
-        "decompress_base")
+        "decompress_base", "encode_edits")
 ]
 
 _lib = None
@@ -783,3 +783,23 @@ def decompress_base(topo: GridTopology, symbols, literals, xi: float, dtype=np.f
     if timing is not None:
         timing["device_ms"] = ms.value
     return out
+
+
+# ---------------------------------------------------------------- edit-set encoding
+def encode_edits(edits: EditSet, codec: int = 1, timing: Optional[dict] = None) -> bytes:
+    """encode_edits<T> (edit_codec.cpp:188-222): the archive's edit payload, byte-identical
+    to the reference; codec 0 = store, 1 = raw DEFLATE."""
+    idx = np.ascontiguousarray(edits.indices, np.uint64)
+    val = np.ascontiguousarray(edits.values)
+    out = C.POINTER(C.c_uint8)()
+    n = C.c_uint64()
+    ms = C.c_double()
+    lib = library()
+    _check(getattr(lib, f"mssz_cu_encode_edits_{_suf(val.dtype)}")(
+        _p(idx) if idx.size else None, _p(val) if val.size else None, C.c_uint64(idx.size), codec,
+        C.byref(out), C.byref(n), C.byref(ms)))
+    data = C.string_at(out, n.value)
+    lib.mssz_cu_free(C.cast(out, C.c_void_p))
+    if timing is not None:
+        timing["device_ms"] = ms.value
+    return data

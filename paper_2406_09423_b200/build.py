@@ -22,7 +22,7 @@ INPUTS_SO = os.path.join(LIBDIR, "libmssz_inputs.so")
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared", "-ldl",
+    "-Xcompiler", "-fPIC", "-shared", "-ldl", "-lz",
 ]
 
 

@@ -1607,3 +1607,4 @@ int mssz_cu_classify_critical(uint64_t n, const uint64_t* asc, const uint64_t* d
 #include "shard_api.cuh"
 #include "verify.cuh"
 #include "base_codec.cuh"
+#include "edit_codec.cuh"
