@@ -115,8 +115,15 @@ __global__ void k_byte_hist(const uint8_t* __restrict__ b, uint64_t L, unsigned 
   for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
   __syncthreads();
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < L; i += stride)
-    atomicAdd(&h[b[i]], 1u);
+  // the stream is dominated by a few byte values: one shared atomic per
+  // distinct value per warp (__match_any_sync groups equal lanes)
+  for (uint64_t wb = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) & ~uint64_t(31); wb < L;
+       wb += stride) {
+    const uint64_t i = wb + (threadIdx.x & 31);
+    const uint32_t v = i < L ? b[i] : 256u;
+    const uint32_t same = __match_any_sync(0xffffffffu, v);
+    if (v < 256 && (threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&h[v], static_cast<uint32_t>(__popc(same)));
+  }
   __syncthreads();
   for (int i = threadIdx.x; i < 256; i += blockDim.x)
     if (h[i]) atomicAdd(&hist[i], static_cast<unsigned long long>(h[i]));
@@ -130,22 +137,49 @@ __global__ void k_code_len(const uint8_t* __restrict__ b, uint64_t L, const uint
 }
 
 // MSB-first packing: bit p of the stream is bit (31 - p % 32) of word p / 32
-// (big-endian words, byte-swapped when copied out).
-__global__ void k_bit_pack(const uint8_t* __restrict__ b, uint64_t L, const uint64_t* __restrict__ code,
-                           const uint8_t* __restrict__ clen, const uint64_t* __restrict__ boff,
-                           uint32_t* __restrict__ words) {
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < L; i += stride) {
-    const uint8_t s = b[i];
-    const int l = clen[s];
-    const uint64_t p = boff[i];
-    const uint64_t w0 = p >> 5;
-    const int b0 = static_cast<int>(p & 31);
-    const unsigned __int128 v = static_cast<unsigned __int128>(code[s]) << (128 - l - b0);
+// (big-endian words, byte-swapped when copied out).  A CTA packs a chunk of
+// kPackChunk consecutive symbols into shared-memory words (shared atomics),
+// then stores its interior words directly and ORs only its two edge words.
+constexpr int kPackChunk = 2048;
+constexpr int kPackWords = kPackChunk * kMaxCodeLength / 32 + 4;
+__global__ void __launch_bounds__(256) k_bit_pack(const uint8_t* __restrict__ b, uint64_t L,
+                                                  const uint64_t* __restrict__ code,
+                                                  const uint8_t* __restrict__ clen,
+                                                  const uint64_t* __restrict__ boff, uint32_t* __restrict__ words) {
+  __shared__ uint32_t sw[kPackWords];
+  __shared__ uint64_t sc[256];
+  __shared__ uint8_t sl[256];
+  for (int k = threadIdx.x; k < 256; k += blockDim.x) {
+    sc[k] = code[k];
+    sl[k] = clen[k];
+  }
+  __syncthreads();
+  for (uint64_t c0 = static_cast<uint64_t>(blockIdx.x) * kPackChunk; c0 < L;
+       c0 += static_cast<uint64_t>(gridDim.x) * kPackChunk) {
+    const uint64_t c1 = min(c0 + kPackChunk, L);
+    const uint64_t wbase = boff[c0] >> 5;
+    const uint64_t wend = (boff[c1 - 1] + sl[b[c1 - 1]] + 31) >> 5;  // exclusive
+    const int nw = static_cast<int>(wend - wbase);
+    __syncthreads();  // the previous chunk's words are written out
+    for (int k = threadIdx.x; k < nw + 4; k += blockDim.x) sw[k] = 0u;
+    __syncthreads();
+    for (uint64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+      const uint8_t s = b[i];
+      const int l = sl[s];
+      const uint64_t p = boff[i] - (wbase << 5);
+      const uint64_t w0 = p >> 5;
+      const int b0 = static_cast<int>(p & 31);
+      const unsigned __int128 v = static_cast<unsigned __int128>(sc[s]) << (128 - l - b0);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t part = static_cast<uint32_t>(v >> (96 - 32 * k));
-      if (part) atomicOr(&words[w0 + k], part);
+      for (int k = 0; k < 3; ++k) {
+        const uint32_t part = static_cast<uint32_t>(v >> (96 - 32 * k));
+        if (part) atomicOr(&sw[w0 + k], part);
+      }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < nw; k += blockDim.x) {
+      if (k == 0 || k == nw - 1) atomicOr(&words[wbase + k], sw[k]);  // shared with neighbour chunks
+      else words[wbase + k] = sw[k];
     }
   }
 }
@@ -261,6 +295,12 @@ void encode_edits_entry(const uint64_t* idx, const T* val, uint64_t n, int codec
     Workspace& ws = workspace(-1);
     std::lock_guard<std::mutex> lk(ws.mu);
     cudaStream_t s = ws.stream;
+    {  // keep freed temporaries in the stream-ordered pool across the syncs below
+      cudaMemPool_t pool;
+      CK(cudaDeviceGetDefaultMemPool(&pool, ws.device));
+      uint64_t keep = ~uint64_t(0);
+      CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    }
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
@@ -374,7 +414,8 @@ void encode_edits_entry(const uint64_t* idx, const T* val, uint64_t n, int codec
     const uint64_t nwords = (nbits + 31) / 32 + 4, nbytes = (nbits + 7) / 8;
     uint32_t* d_words = dalloc<uint32_t>(nwords, s);
     CK(cudaMemsetAsync(d_words, 0, 4 * nwords, s));
-    k_bit_pack<<<bL2, 256, 0, s>>>(d_c, L2, d_code, d_clen, d_boff, d_words);
+    k_bit_pack<<<grid_for((L2 + kPackChunk - 1) / kPackChunk, 1, ws.sms, 8), 256, 0, s>>>(d_c, L2, d_code, d_clen,
+                                                                                           d_boff, d_words);
     uint8_t* d_body = dalloc<uint8_t>(nbytes, s);
     k_bswap_words<<<grid_for(nbytes, 256, ws.sms, 8), 256, 0, s>>>(d_words, nbytes, d_body);
     CK_LAUNCH();
