@@ -149,6 +149,7 @@ struct Workspace {
   int device = 0;
   int sms = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // H2D of fhat overlapping the f-side setup
   DevBuf f, g, fh, fdir, gdir, touched, stamp, fmark, lab, fin, lists, tiles;
   DevBuf tE, tEcnt, toldfin, tdirty, taffected, tbits, tcnt, tlist;  // label-tile store
   DevBuf xbuf;  // sparse R pass: crossing lists X (2 families x 2 buffers)
@@ -175,6 +176,7 @@ struct Workspace {
     CK(cudaSetDevice(dev));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
     CK(cudaMalloc(&ctl, sizeof(Ctl)));
     CK(cudaMallocHost(&hctl, sizeof(Ctl)));
     for (auto& e : ev) CK(cudaEventCreate(&e));
@@ -197,6 +199,7 @@ struct Workspace {
     if (ctl) cudaFree(ctl);
     if (hctl) cudaFreeHost(hctl);
     if (stream) cudaStreamDestroy(stream);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
     ctl = nullptr;
     hctl = nullptr;
     stream = nullptr;
@@ -1025,10 +1028,24 @@ struct Engine {
 
   // Validation + EditState ctor + outer loop + tripwire (edit_engine.cpp:386-428).
   // d_f: original (device), g already holds fhat.
-  void run(const T* d_f, double xi) {
+  // fh_ready (optional): g is still being filled (H2D of fhat on the copy
+  // stream); the f-side setup -- f's directions and labels, which the
+  // reference computes in the EditState ctor -- runs first and overlaps it.
+  void run(const T* d_f, double xi, cudaEvent_t fh_ready = nullptr) {
     if (!(xi > 0.0)) fail(MSSZ_CU_ERR_USAGE, "derive_edits requires xi > 0");
     bind(d_f);
     s.xi = xi;
+    if (fh_ready) {
+      CK(cudaEventRecord(ws.ev[0], ws.stream));
+      directions(d_f, ws.fdir.as<uint8_t>());
+      CK(cudaEventRecord(ws.ev[1], ws.stream));
+      label_pass(s.fdir, lab(0), lab(1), false, true);
+      float ms = 0;
+      CK(cudaEventSynchronize(ws.ev[1]));
+      CK(cudaEventElapsedTime(&ms, ws.ev[0], ws.ev[1]));
+      dir_ms += ms;
+      CK(cudaStreamWaitEvent(ws.stream, fh_ready, 0));
+    }
     reset_ctl();
     ws.push_ctl();
     pre(kProfValidate);
@@ -1047,12 +1064,13 @@ struct Engine {
     // EditState ctor (edit_engine.cpp:36-56)
     s.touched = nullptr;  // touched == (g != fhat), derived by edit_flags()
     CK(cudaEventRecord(ws.ev[0], ws.stream));
-    directions(d_f, ws.fdir.as<uint8_t>());
+    if (!fh_ready) directions(d_f, ws.fdir.as<uint8_t>());
     directions(s.g, s.gdir);
     CK(cudaEventRecord(ws.ev[1], ws.stream));
-    label_pass(s.fdir, lab(0), lab(1), false, true);
+    if (!fh_ready) label_pass(s.fdir, lab(0), lab(1), false, true);
     {
       float ms = 0;
+      CK(cudaEventSynchronize(ws.ev[1]));
       CK(cudaEventElapsedTime(&ms, ws.ev[0], ws.ev[1]));
       dir_ms += ms;
     }
@@ -1169,12 +1187,16 @@ void derive_host(int ndims, const uint64_t* dims, const T* f, const T* fh, doubl
   EvGuard guard{evs};
   CK(cudaEventRecord(t0, ws.stream));
   ws.fh.ensure(sizeof(T) * ((geo.n + 63) & ~uint64_t(63)));
+  // f first on the engine stream; fhat on the copy stream while f's directions
+  // and labels are computed (Engine::run with fh_ready)
   CK(cudaMemcpyAsync(ws.f.p, f, sizeof(T) * geo.n, cudaMemcpyHostToDevice, ws.stream));
-  CK(cudaMemcpyAsync(ws.fh.p, fh, sizeof(T) * geo.n, cudaMemcpyHostToDevice, ws.stream));
-  CK(cudaMemcpyAsync(ws.g.p, ws.fh.p, sizeof(T) * geo.n, cudaMemcpyDeviceToDevice, ws.stream));
-  CK(cudaEventRecord(t1, ws.stream));
+  CK(cudaEventRecord(t2, ws.stream));  // f is in: fhat follows on the copy engine
+  CK(cudaStreamWaitEvent(ws.copy_stream, t2, 0));
+  CK(cudaMemcpyAsync(ws.fh.p, fh, sizeof(T) * geo.n, cudaMemcpyHostToDevice, ws.copy_stream));
+  CK(cudaMemcpyAsync(ws.g.p, ws.fh.p, sizeof(T) * geo.n, cudaMemcpyDeviceToDevice, ws.copy_stream));
+  CK(cudaEventRecord(t1, ws.copy_stream));
   eng.fhat = ws.fh.as<T>();
-  eng.run(ws.f.as<T>(), xi);
+  eng.run(ws.f.as<T>(), xi, t1);
   const uint64_t count = eng.compact(eng.edit_flags(), 1, eng.s.g, eng.edit_idx(), eng.edit_val());
   CK(cudaEventRecord(t2, ws.stream));
   uint64_t* hi = idx_buf;
