@@ -56,7 +56,9 @@ def alg_bytes(cls: str, es: int, n: int, st, launches: int) -> float:
         "detect_kind": 2 * n * launches,                 # full sweeps: fdir + gdir
         "label_init": 9 * tile * st.label_tiles,         # code byte in, two u32 labels out per tile vertex
         "label_finish": 16 * n * launches,               # two labels read + gathered (f labels once)
-        "rfix": 2 * tile * st.rfix_tiles,                # lower bound: both codes of every listed tile vertex
+        # both codes of every listed tile vertex; per divergent (vertex, family):
+        # provisional label, its final (one gather) and the f label
+        "rfix": 2 * tile * st.rfix_tiles + 12 * st.rfix_divergent,
         "compact": 2 * n * launches,                     # flag sweep (count + write passes)
     }.get(cls, 0.0)
 

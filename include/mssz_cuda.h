@@ -119,6 +119,7 @@ typedef struct mssz_cu_stats {
   uint64_t rfix_tiles;        /* label tiles whose mismatch bits were recomputed */
   uint64_t sparse_iterations; /* R iterations resolved by the sparse Up(X) pass */
   uint64_t sparse_up;         /* sum of |Up(X)| over sparse passes */
+  uint64_t rfix_divergent;    /* (vertex, family) pairs k_rfix_tiles resolved a label for */
   uint64_t kernel_count[MSSZ_CU_PROF_CLASSES]; /* launches per kernel class */
   double kernel_ms[MSSZ_CU_PROF_CLASSES];      /* device ms per class (profile = 1 only) */
 } mssz_cu_stats;

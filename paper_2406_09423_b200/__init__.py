@@ -153,6 +153,7 @@ class EditStats:
     rfix_tiles: int = 0
     sparse_iterations: int = 0
     sparse_up: int = 0
+    rfix_divergent: int = 0
     kernel_count: list = field(default_factory=lambda: [0] * 16)
     kernel_ms: list = field(default_factory=lambda: [0.0] * 16)
 
@@ -250,7 +251,7 @@ class _Stats(C.Structure):
         ("detect_sweeps", C.c_uint64), ("frontier_vertices", C.c_uint64),
         ("kernel_launches", C.c_uint64), ("big_batches", C.c_uint64),
         ("huge_batches", C.c_uint64), ("label_tiles", C.c_uint64), ("rfix_tiles", C.c_uint64),
-        ("sparse_iterations", C.c_uint64), ("sparse_up", C.c_uint64),
+        ("sparse_iterations", C.c_uint64), ("sparse_up", C.c_uint64), ("rfix_divergent", C.c_uint64),
         ("kernel_count", C.c_uint64 * 16), ("kernel_ms", C.c_double * 16),
     ]
 

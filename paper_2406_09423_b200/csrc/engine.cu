@@ -623,6 +623,7 @@ struct Engine {
     }
     CK(cudaMemsetAsync(ts.dirty, 0, ts.ntiles, ws.stream));
     ws.pull_ctl();
+    st.rfix_divergent += ws.hctl->rfix_div;
     if (raise_trouble && ws.hctl->status == kStatusTroubleMax)
       fail(MSSZ_CU_ERR_INTERNAL, "troublemaker target is an extremum (stale critical report)");
     return ws.hctl->mism;
@@ -770,8 +771,8 @@ struct Engine {
       fail(MSSZ_CU_ERR_NON_CONVERGENCE, "%s subloop stalled at the float floor", kKindName[kind]);
     if (trace)
       std::fprintf(stderr,
-                   "[mssz] C kind=%d iters=%llu edits=%llu big=%llu frontier=%llu small_ms=%.2f big_ms=%.2f\n",
-                   kind, (unsigned long long)c.iters, (unsigned long long)c.edits,
+                   "[mssz] C kind=%d iters=%llu edits=%llu items=%llu big=%llu frontier=%llu small_ms=%.2f big_ms=%.2f\n",
+                   kind, (unsigned long long)c.iters, (unsigned long long)c.edits, (unsigned long long)c.items,
                    (unsigned long long)c.big_batches, (unsigned long long)c.frontier,
                    c.small_ns * 1e-6, c.big_ns * 1e-6);
     if (trace && c.big_batches)

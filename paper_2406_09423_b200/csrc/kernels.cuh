@@ -42,6 +42,8 @@ struct Ctl {
   uint32_t sp_abort;
   uint32_t sp_levels;
   uint32_t bnd[2];       // z-slab sharding: boundary edits packed for rank-1 / rank+1
+  uint64_t items;        // Σ worklist sizes over the batches of a subloop (trace)
+  uint64_t rfix_div;     // k_rfix_tiles: divergent (vertex, family) pairs evaluated
 };
 
 enum : uint32_t {
@@ -1158,7 +1160,7 @@ __global__ void __launch_bounds__(kSubThreads, 2)
 
   uint32_t cur = *reinterpret_cast<volatile uint32_t*>(&ctl->cur);
   uint64_t attempted = *reinterpret_cast<volatile uint64_t*>(&ctl->attempted);
-  uint64_t iters = 0, edits = 0, frontier = 0, big = 0, small_ns = 0, big_ns = 0;
+  uint64_t iters = 0, edits = 0, frontier = 0, big = 0, small_ns = 0, big_ns = 0, items = 0;
   uint32_t status = kStatusOk, done = 0, seq = 0;
   for (;;) {
     const uint32_t n = *reinterpret_cast<volatile uint32_t*>(&ctl->list_count[cur]);
@@ -1208,6 +1210,7 @@ __global__ void __launch_bounds__(kSubThreads, 2)
     ++iters;
     edits += r.applied;
     frontier += r.nf;
+    items += n;
     cur ^= 1;
     ++done;
   }
@@ -1224,6 +1227,7 @@ __global__ void __launch_bounds__(kSubThreads, 2)
     ctl->edits += edits;
     ctl->frontier += frontier;
     ctl->big_batches += big;
+    ctl->items += items;
     ctl->small_ns += small_ns;
     ctl->big_ns += big_ns;
     ctl->status = status;
@@ -1374,6 +1378,7 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
   }
   __syncthreads();
   // local parents; a chain that leaves the tile stops at its last inside vertex
+  uint32_t own[PER];
 #pragma unroll
   for (int j = 0; j < PER; ++j) {
     const int i = threadIdx.x + j * kLabelTileThreads;
@@ -1387,18 +1392,21 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
     const uint32_t ca = code & 15u, cd = code >> 4;
     const uint32_t pa = (sface[ca] & on) ? i : i + sloc[ca];  // SELF: sloc 0
     const uint32_t pd = (sface[cd] & on) ? i : i + sloc[cd];
-    ptr[i] = pa | (pd << 16);
+    own[j] = pa | (pd << 16);
+    ptr[i] = own[j];
   }
   __syncthreads();
-  // in-place doubling on both families at once
+  // in-place doubling on both families at once; a thread's own pointers live
+  // in registers (only this thread writes them), the others are read from smem
   for (;;) {
     bool changed = false;
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
       const int i = threadIdx.x + j * kLabelTileThreads;
-      const uint32_t p = ptr[i];
+      const uint32_t p = own[j];
       const uint32_t np = (ptr[p & 0xFFFFu] & 0xFFFFu) | (ptr[p >> 16] & 0xFFFF0000u);
       if (np != p) {
+        own[j] = np;
         ptr[i] = np;
         changed = true;
       }
@@ -1413,7 +1421,7 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
     const int i = threadIdx.x + j * kLabelTileThreads;
     const int lx = i & (TL::TX - 1), ly = (i >> TL::LX) & (TL::TY - 1), lz = i >> (TL::LX + TL::LY);
     if (lx < ex && ly < ey && lz < ez) {
-      const uint32_t p = ptr[i];
+      const uint32_t p = own[j];
       const uint32_t gi = rowbase[i >> TL::LX] + lx;
 #pragma unroll
       for (int fam = 0; fam < 2; ++fam) {
@@ -1692,7 +1700,7 @@ __global__ void __launch_bounds__(256) k_rfix_tiles(State<T> s, const uint32_t* 
   const int ez = DIM == 2 ? 1 : min(TL::TZ, static_cast<int>(g.Z - z0));
   const uint32_t base = x0 + g.X * y0 + g.XY * z0;
   uint32_t* bits = ts.mis_bits + static_cast<size_t>(b) * 2 * (kLabelTileN / 32);
-  uint32_t cnt = 0;
+  uint32_t cnt = 0, ndiv = 0;
   for (int i = threadIdx.x; i < kLabelTileN; i += blockDim.x) {
     const int lx = i & (TL::TX - 1), ly = (i >> TL::LX) & (TL::TY - 1), lz = i >> (TL::LX + TL::LY);
     bool ma = false, md = false;
@@ -1712,6 +1720,7 @@ __global__ void __launch_bounds__(256) k_rfix_tiles(State<T> s, const uint32_t* 
       }
       ma = wa && resolve_label(sr, __ldg(finM + la), 0) != fa;
       md = wd && resolve_label(sr, __ldg(finm + ld), 1) != fd;
+      ndiv += (wa ? 1u : 0u) + (wd ? 1u : 0u);
     }
     const uint32_t wa_bits = __ballot_sync(0xffffffffu, ma);
     const uint32_t wd_bits = __ballot_sync(0xffffffffu, md);
@@ -1721,12 +1730,16 @@ __global__ void __launch_bounds__(256) k_rfix_tiles(State<T> s, const uint32_t* 
       cnt += __popc(wa_bits) + __popc(wd_bits);
     }
   }
-  __shared__ uint32_t scnt;
-  if (threadIdx.x == 0) scnt = 0;
+  __shared__ uint32_t scnt, sdiv;
+  if (threadIdx.x == 0) scnt = sdiv = 0;
   __syncthreads();
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&scnt, cnt);
+  if (ndiv) atomicAdd(&sdiv, ndiv);
   __syncthreads();
-  if (threadIdx.x == 0) ts.mis_cnt[b] = scnt;
+  if (threadIdx.x == 0) {
+    ts.mis_cnt[b] = scnt;
+    if (sdiv) atomicAdd(reinterpret_cast<unsigned long long*>(&s.ctl->rfix_div), static_cast<unsigned long long>(sdiv));
+  }
 }
 
 // Targets of the R batch from the mismatch bitmaps of the listed tiles
