@@ -1751,24 +1751,45 @@ __global__ void __launch_bounds__(256) k_expand_targets(State<T> s, const uint32
                                                         TileStore ts, uint32_t* __restrict__ targets,
                                                         uint32_t* count) {
   using TL = LabelTile<DIM>;
+  constexpr int NW = 2 * (kLabelTileN / 32);  // bitmap words per tile (both families)
   const Geom& g = s.geo;
   const uint32_t ntx = (g.X + TL::TX - 1) / TL::TX;
   const uint32_t nty = (g.Y + TL::TY - 1) / TL::TY;
   const uint32_t b = tiles[blockIdx.x];
   const uint32_t tx = b % ntx, ty = (b / ntx) % nty, tz = b / (ntx * nty);
   const uint32_t base = tx * TL::TX + g.X * (ty * TL::TY) + g.XY * (tz * TL::TZ);
-  const uint32_t* bits = ts.mis_bits + static_cast<size_t>(b) * 2 * (kLabelTileN / 32);
-  uint32_t mism = 0;
-  for (int w = threadIdx.x; w < 2 * (kLabelTileN / 32); w += blockDim.x) {  // warp-uniform trip count
-    uint32_t word = bits[w];
-    const int fam = w >= kLabelTileN / 32;
-    mism += __popc(word);
-    const uint32_t pos0 = warp_reserve(__popc(word), count);
-    uint32_t pos = pos0;
-    while (word) {
-      const int j = __ffs(word) - 1;
-      word &= word - 1;
-      const int i = ((w % (kLabelTileN / 32)) << 5) + j;
+  const uint32_t* bits = ts.mis_bits + static_cast<size_t>(b) * NW;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int wpw = NW / nwarps;  // words per warp, contiguous
+  // one reservation per tile: per-warp counts, scanned in shared memory
+  __shared__ uint32_t wsum[32];
+  __shared__ uint32_t tbase;
+  uint32_t c = 0;
+  for (int k = lane; k < wpw; k += 32) c += __popc(__ldg(bits + warp * wpw + k));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) wsum[warp] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < nwarps; ++w) {
+      const uint32_t x = wsum[w];
+      wsum[w] = t;
+      t += x;
+    }
+    tbase = t ? atomicAdd(count, t) : 0u;
+    if (t) atomicAdd(reinterpret_cast<unsigned long long*>(&s.ctl->mism), static_cast<unsigned long long>(t));
+  }
+  __syncthreads();
+  uint32_t pos = tbase + wsum[warp];
+  // lane j expands bit j of each of the warp's words, in word order
+#pragma unroll 4
+  for (int k = 0; k < wpw; ++k) {
+    const int w = warp * wpw + k;
+    const uint32_t word = __ldg(bits + w);
+    if ((word >> lane) & 1u) {
+      const int fam = w >= kLabelTileN / 32;
+      const int i = ((w % (kLabelTileN / 32)) << 5) + lane;
       const int lx = i & (TL::TX - 1), ly = (i >> TL::LX) & (TL::TY - 1), lz = i >> (TL::LX + TL::LY);
       const uint32_t v = base + lx + g.X * ly + g.XY * lz;
       const uint32_t code = fam ? (__ldg(s.fdir + v) >> 4) : (__ldg(s.gdir + v) & 15u);
@@ -1777,14 +1798,10 @@ __global__ void __launch_bounds__(256) k_expand_targets(State<T> s, const uint32
       const uint32_t t = code == kSelf ? v : v + g.off[code];
       // owner-computes (z-slab windows): only targets this rank owns; on a
       // single device every target is owned.  A dropped slot keeps the list dense.
-      targets[pos++] = t - s.own_lo < s.own_n ? t : kNoTarget;
+      targets[pos + __popc(word & ((1u << lane) - 1u))] = t - s.own_lo < s.own_n ? t : kNoTarget;
     }
+    pos += __popc(word);
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mism += __shfl_xor_sync(0xffffffffu, mism, o);
-  if ((threadIdx.x & 31) == 0 && mism)
-    atomicAdd(reinterpret_cast<unsigned long long*>(&s.ctl->mism),
-              static_cast<unsigned long long>(mism));
 }
 
 // ---------------------------------------------------------------------------
