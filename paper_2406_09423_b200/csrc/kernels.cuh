@@ -1530,8 +1530,8 @@ __global__ void __launch_bounds__(256) k_exit_jump_tiles(TileStore ts, uint32_t*
     const uint32_t n = ts.Ecnt[b * 2 + fam];
     const size_t o = (static_cast<size_t>(b) * 2 + fam) * ts.surface;
     uint32_t* fin = fam ? finm : finM;
-    for (uint32_t kb = threadIdx.x & ~31u; kb < n; kb += blockDim.x) {
-      const uint32_t k = kb + (threadIdx.x & 31);
+    for (uint32_t kb = 0; kb < n; kb += blockDim.x) {  // block-uniform (block_reserve)
+      const uint32_t k = kb + threadIdx.x;
       bool keep = false;
       uint32_t e = 0;
       if (k < n) {
@@ -1543,7 +1543,8 @@ __global__ void __launch_bounds__(256) k_exit_jump_tiles(TileStore ts, uint32_t*
           keep = fin[ll] != ll;
         }
       }
-      warp_append(keep, e, fam ? out_d : out_a, cnt_out + fam);
+      const uint32_t pos = block_reserve(keep ? 1u : 0u, cnt_out + fam);  // one atomic per block step
+      if (keep) (fam ? out_d : out_a)[pos] = e;
     }
   }
 }
