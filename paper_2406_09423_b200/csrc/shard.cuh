@@ -643,7 +643,7 @@ struct SlabEngine {
     CK(cudaMemsetAsync(ws.ctl->bnd, 0, sizeof(uint32_t) * 2, ws.stream));
     const uint32_t lo_end = own_lo + 2 * XY, hi_begin = own_hi - 2 * XY;
     eng.pre(kProfFix);
-    k_pack_boundary<T><<<blocks(n() / 64 + 1), 256, 0, ws.stream>>>(
+    k_pack_boundary<T><<<ws.sms, 256, 0, ws.stream>>>(  // grid-stride over |S| (device count)
         s(), lo_end, hi_begin, pl.r > 0, pl.r + 1 < pl.P, base, sb.send[0].as<BEdit<T>>(),
         sb.send[1].as<BEdit<T>>());
     eng.launched(kProfFix);
@@ -785,7 +785,8 @@ struct SlabEngine {
     CK(cudaMemsetAsync(&ws.ctl->s_count, 0, sizeof(uint32_t) * 2, ws.stream));  // s_count, f_count
     CK(cudaMemsetAsync(&ws.ctl->retry_count, 0, sizeof(uint32_t), ws.stream));
     eng.pre(kProfFix);
-    k_slab_fix<T><<<blocks(n() / 8 + 1, 4), 256, 0, ws.stream>>>(s(), list, count, rule, batch,
+    // grid-stride over a device-side count: 2 CTAs per SM whatever the batch size
+    k_slab_fix<T><<<2 * ws.sms, 256, 0, ws.stream>>>(s(), list, count, rule, batch,
                                                                    retry ? s().F : nullptr,
                                                                    retry ? &ws.ctl->retry_count : nullptr);
     eng.launched(kProfFix);
