@@ -119,12 +119,22 @@ struct Api<float> {
   static constexpr auto derive = mssz_cu_derive_edits_f32;
   static constexpr auto directions = mssz_cu_compute_directions_f32;
   static constexpr auto apply = mssz_cu_apply_edits_f32;
+  static constexpr auto verify = mssz_cu_verify_f32;
+  static constexpr auto segmentation = mssz_cu_segmentation_f32;
+  static constexpr auto compress_base = mssz_cu_compress_base_f32;
+  static constexpr auto decompress_base = mssz_cu_decompress_base_f32;
+  static constexpr auto encode_edits = mssz_cu_encode_edits_f32;
 };
 template <>
 struct Api<double> {
   static constexpr auto derive = mssz_cu_derive_edits_f64;
   static constexpr auto directions = mssz_cu_compute_directions_f64;
   static constexpr auto apply = mssz_cu_apply_edits_f64;
+  static constexpr auto verify = mssz_cu_verify_f64;
+  static constexpr auto segmentation = mssz_cu_segmentation_f64;
+  static constexpr auto compress_base = mssz_cu_compress_base_f64;
+  static constexpr auto decompress_base = mssz_cu_decompress_base_f64;
+  static constexpr auto encode_edits = mssz_cu_encode_edits_f64;
 };
 template <class T>
 void batch_trampoline(const void* g, std::uint64_t n, void* user) {
@@ -195,6 +205,130 @@ std::vector<T> apply_edits(const GridTopology& topo, const T* decompressed,
   std::vector<T> out(topo.vertex_count);
   check(detail::Api<T>::apply(topo.vertex_count, decompressed, edits.indices.data(),
                               edits.values.data(), edits.size(), out.data()));
+  return out;
+}
+
+// ---- the `mss` subcommand (tools/mssz.cpp:260-266) -------------------------
+// compute_labels(compute_directions(values)) as one device pass.
+template <class T>
+SegmentationLabels segmentation(const GridTopology& topo, const T* values) {
+  SegmentationLabels l;
+  l.max_label.resize(topo.vertex_count);
+  l.min_label.resize(topo.vertex_count);
+  check(detail::Api<T>::segmentation(topo.ndims, topo.dims.data(), values, l.max_label.data(),
+                                     l.min_label.data()));
+  return l;
+}
+
+// ---- verification report (metrics.hpp:14-24, tools/mssz.cpp:84-104) --------
+struct VerificationReport {
+  double mss_distortion = 0.0;
+  double right_labeled_ratio = 1.0;
+  double psnr = 0.0;
+  double edit_ratio = 0.0;
+  double ocr = 0.0;
+  double obr = 0.0;
+  std::uint64_t bound_violations = 0;
+  std::uint64_t fp_max = 0, fp_min = 0, fn_max = 0, fn_min = 0;
+  // B200 extras: raw mismatch count and the device time of the report.
+  std::uint64_t mismatches = 0;
+  double device_seconds = 0.0;
+};
+
+// build_report<T>(original, candidate, xi, edit_count, archive_bytes, policy)
+// (tools/mssz.cpp:84-104); `device` replaces the ExecPolicy.
+template <class T>
+VerificationReport build_report(const GridTopology& topo, const T* original, const T* candidate,
+                                double xi, std::uint64_t edit_count = 0,
+                                std::uint64_t archive_bytes = 0, int device = -1) {
+  mssz_cu_options o;
+  mssz_cu_default_options(&o);
+  o.device = device;
+  mssz_cu_report r{};
+  check(detail::Api<T>::verify(topo.ndims, topo.dims.data(), original, candidate, xi,
+                               edit_count, archive_bytes, &o, &r));
+  VerificationReport v;
+  v.mss_distortion = r.mss_distortion;
+  v.right_labeled_ratio = r.right_labeled_ratio;
+  v.psnr = r.psnr;
+  v.edit_ratio = r.edit_ratio;
+  v.ocr = r.ocr;
+  v.obr = r.obr;
+  v.bound_violations = r.bound_violations;
+  v.fp_max = r.fp_max;
+  v.fp_min = r.fp_min;
+  v.fn_max = r.fn_max;
+  v.fn_min = r.fn_min;
+  v.mismatches = r.mismatches;
+  v.device_seconds = r.device_seconds;
+  return v;
+}
+
+// The reference CLI's `verify` verdict (tools/mssz.cpp: exit 0 iff both are 0).
+inline bool verified(const VerificationReport& r) {
+  return r.mss_distortion == 0.0 && r.bound_violations == 0;
+}
+
+// ---- base codec (base_codec.hpp:29-40) --------------------------------------
+// The reference's compress_base returns {payload, reconstruction}; the payload is
+// huffman::encode_stream(symbols) followed by the literals.  The GPU computes the
+// prediction/quantisation wavefront, so this returns the reconstruction together
+// with the symbol stream (0 = escape, else 1 + zigzag(q)) and the escaped literals
+// in index order — the inputs of the reference's Huffman framing.
+template <class T>
+struct BaseQuantization {
+  std::vector<T> reconstruction;  // fhat, |f - fhat| <= xi pointwise
+  std::vector<std::uint32_t> symbols;
+  std::vector<T> literals;
+  double device_ms = 0.0;
+};
+
+template <class T>
+BaseQuantization<T> compress_base(const GridTopology& topo, const T* values, double xi) {
+  BaseQuantization<T> q;
+  q.reconstruction.resize(topo.vertex_count);
+  q.symbols.resize(topo.vertex_count);
+  std::uint64_t escapes = 0;
+  check(detail::Api<T>::compress_base(topo.ndims, topo.dims.data(), values, xi,
+                                      q.reconstruction.data(), q.symbols.data(), &escapes,
+                                      &q.device_ms));
+  q.literals.reserve(escapes);
+  for (std::uint64_t v = 0; v < topo.vertex_count; ++v)
+    if (q.symbols[v] == 0) q.literals.push_back(values[v]);
+  if (q.literals.size() != escapes)
+    throw Error(ErrKind::internal, "compress_base: escape count mismatch");
+  return q;
+}
+
+// decompress_base<T> (base_codec.hpp:38-40) after the Huffman decode of the payload.
+template <class T>
+std::vector<T> decompress_base(const GridTopology& topo, std::span<const std::uint32_t> symbols,
+                               std::span<const T> literals, double xi) {
+  if (symbols.size() != topo.vertex_count)
+    throw Error(ErrKind::corrupt_archive, "code count does not match the grid");
+  std::vector<T> out(topo.vertex_count);
+  check(detail::Api<T>::decompress_base(topo.ndims, topo.dims.data(), symbols.data(),
+                                        literals.empty() ? nullptr : literals.data(),
+                                        literals.size(), xi, out.data(), nullptr));
+  return out;
+}
+
+// ---- edit-set encoding (edit_codec.hpp:29-43) --------------------------------
+enum class BackendCodec : std::uint8_t { store = 0, deflate = 1 };
+
+// encode_edits<T>(edits, codec): byte-identical to the reference's payload.
+template <class T>
+std::vector<std::uint8_t> encode_edits(const EditSet<T>& edits, BackendCodec codec) {
+  if (edits.indices.size() != edits.values.size())
+    throw Error(ErrKind::usage, "edit set index/value length mismatch");
+  std::uint8_t* buf = nullptr;
+  std::uint64_t len = 0;
+  check(detail::Api<T>::encode_edits(edits.indices.empty() ? nullptr : edits.indices.data(),
+                                     edits.values.empty() ? nullptr : edits.values.data(),
+                                     edits.size(), static_cast<int>(codec), &buf, &len,
+                                     nullptr));
+  std::vector<std::uint8_t> out(buf, buf + len);
+  mssz_cu_free(buf);
   return out;
 }
 

@@ -30,7 +30,14 @@ def test_cpp_example_fails_loudly_without_gpu(mssz, example):
 
 
 @pytest.mark.gpu
-def test_cpp_example_on_gpu(mssz, example):
-    r = subprocess.run([example], capture_output=True, text=True, timeout=120)
+def test_cpp_example_on_gpu(mssz, example, tmp_path, ref_lib):
+    r = subprocess.run([example, str(tmp_path)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, (r.stdout, r.stderr)
     assert r.stdout.startswith("ok")
+    # the payload the C++ binding produced equals the reference encoder's bytes
+    import numpy as np
+    idx = np.fromfile(tmp_path / "indices.u64", np.uint64)
+    val = np.fromfile(tmp_path / "values.f32", np.float32)
+    payload = (tmp_path / "payload.bin").read_bytes()
+    assert idx.size > 0
+    assert payload == ref_lib.encode_edits(idx, val, 1)
