@@ -740,8 +740,9 @@ struct Engine {
     uint32_t maxb = opt.on_batch ? 1u : 0xFFFFFFFFu;
     uint32_t small_max = kSmallBatchMax;
     uint32_t huge_min = std::max<uint32_t>(kSmallBatchMax, n() / kHugeBatchDivisor);
+    uint32_t park_cap = (n() + 63) & ~63u;  // P lives in list(3) (State::F)
     void* args[] = {&s, &kind, &cap, (void*)&batch_base, (void*)&mark_base, &maxb, &small_max,
-                    &huge_min};
+                    &huge_min, &park_cap};
     void* fn = geo.ndims == 2 ? (void*)k_subloop<T, 2> : (void*)k_subloop<T, 3>;
     const int blocks = coop_grid();
     uint64_t seen_iters = 0;
@@ -771,8 +772,9 @@ struct Engine {
       fail(MSSZ_CU_ERR_NON_CONVERGENCE, "%s subloop stalled at the float floor", kKindName[kind]);
     if (trace)
       std::fprintf(stderr,
-                   "[mssz] C kind=%d iters=%llu edits=%llu items=%llu big=%llu frontier=%llu small_ms=%.2f big_ms=%.2f\n",
+                   "[mssz] C kind=%d iters=%llu edits=%llu items=%llu merges=%llu big=%llu frontier=%llu small_ms=%.2f big_ms=%.2f\n",
                    kind, (unsigned long long)c.iters, (unsigned long long)c.edits, (unsigned long long)c.items,
+                   (unsigned long long)c.merges,
                    (unsigned long long)c.big_batches, (unsigned long long)c.frontier,
                    c.small_ns * 1e-6, c.big_ns * 1e-6);
     if (trace && c.big_batches)

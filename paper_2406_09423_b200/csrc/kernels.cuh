@@ -44,6 +44,8 @@ struct Ctl {
   uint32_t bnd[2];       // z-slab sharding: boundary edits packed for rank-1 / rank+1
   uint64_t items;        // Σ worklist sizes over the batches of a subloop (trace)
   uint64_t rfix_div;     // k_rfix_tiles: divergent (vertex, family) pairs evaluated
+  uint32_t park_count;   // k_subloop: entries of the parked-item list (State::F)
+  uint32_t merges;       // k_subloop: parked-list merges (trace)
 };
 
 enum : uint32_t {
@@ -697,6 +699,10 @@ struct State {
   uint32_t* cstamp;  // per 64-vertex chunk: mark id of the last batch that changed a code in it
 };
 
+// fmark value of a parked worklist item (never a batch mark: marks stay below
+// 0xF0000000, Workspace::ensure)
+constexpr uint32_t kParked = 0xFFFFFFFFu;
+
 // claim (edit_engine.cpp:160-169) + lower_step (:75-86): the first claimant of
 // t in this batch lowers it from the pre-batch value; exactly one winner per
 // target, so Σ winners == the reference's applied count.
@@ -718,7 +724,8 @@ template <class T>
 __device__ __forceinline__ void fix_batch(const State<T>& s, const uint32_t* __restrict__ list,
                                           uint32_t n, int rule, uint32_t batch, uint32_t* s_count,
                                           uint64_t tid, uint64_t stride, uint32_t* retry = nullptr,
-                                          uint32_t* retry_count = nullptr) {
+                                          uint32_t* retry_count = nullptr, uint32_t* park = nullptr,
+                                          uint32_t* park_count = nullptr) {
   // two list items per lane per step: their loads and claims overlap
   const uint64_t step = 2 * stride;
   __shared__ uint32_t sstage[kStageWarps][kStageK * 32], rstage[kStageWarps][kStageK * 32];
@@ -760,13 +767,23 @@ __device__ __forceinline__ void fix_batch(const State<T>& s, const uint32_t* __r
     }
     sbuf.push(ok[0], t[0], s.S, s_count);
     sbuf.push(ok[1], t[1], s.S, s_count);
-    if (retry) {
+    if (park) {  // won the claim, target at its floor: park the item (see k_subloop)
+      bool pk[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        pk[j] = live[j] && prev[j] != batch && !ok[j];
+        if (pk[j]) s.fmark[v[j]] = kParked;
+      }
+      rbuf.push(pk[0], v[0], park, park_count);
+      rbuf.push(pk[1], v[1], park, park_count);
+    } else if (retry) {
       rbuf.push(live[0] && !ok[0], v[0], retry, retry_count);
       rbuf.push(live[1] && !ok[1], v[1], retry, retry_count);
     }
   }
   sbuf.flush(s.S, s_count);
-  if (retry) rbuf.flush(retry, retry_count);
+  if (park) rbuf.flush(park, park_count);
+  else if (retry) rbuf.flush(retry, retry_count);
 }
 
 // Stencil slot k -> (dx, dy, dz) without tables: slots come in (+d, -d) pairs
@@ -884,7 +901,8 @@ __device__ __forceinline__ void rebuild_retry(const uint32_t* __restrict__ retry
     uint32_t v = 0;
     if (i < nr) {
       v = __ldcg(retry + i);
-      keep = __ldcg(fmark + v) != mark;
+      const uint32_t fm = __ldcg(fmark + v);
+      keep = fm != mark && fm != kParked;
     }
     warp_append(keep, v, nxt, nxt_count);
   }
@@ -1033,17 +1051,69 @@ __global__ void __launch_bounds__(256) k_detect_dirty(const uint8_t* __restrict_
 // detect sweep (6 B/vertex) beats ~15 random read-modify-writes per edit.
 // batch ids: batch_base + 2*it (+1 for the FPmin fallback); mark ids: mark_base + it.
 constexpr int kSubThreads = 512;
-enum : uint32_t { kCmdBatch = 1, kCmdExit = 2 };
+enum : uint32_t { kCmdBatch = 1, kCmdExit = 2, kCmdMerge = 3, kCmdFallback = 4 };
+constexpr uint32_t kNeedMerge = 0xFFFFFFFFu;  // BatchResult::applied: merge parked items first
 
 struct BatchResult {
   uint32_t applied;
   uint32_t nf;
 };
 
+// Parked items (k_subloop).  An item that won its claim while its target sat at
+// the floor fails every later batch until its own code is re-evaluated: the
+// target (asc_g(v) or v itself) is fixed while gdir[v] is, and g only falls, so
+// lower_step keeps failing, and it blocks nobody (no claimant can lower a target
+// at its floor).  Such items leave the worklist for the parked list P
+// (fmark[v] = kParked) instead of being re-fixed every batch; a frontier
+// re-evaluation overwrites fmark[v] and re-adds v to the worklist if it is
+// still of the kind, which drops its P entry.  P is merged back whenever the
+// reference's batch would see a different outcome without it: before the
+// FPmin fallback (the fallback runs over the whole list), when the worklist
+// runs empty, and on every exit from the kernel.  Batch outcomes, ids and
+// counts are exactly the reference's.
+//
+// merge: (optionally) clear the parked flag of the first nclear worklist items
+// (parked in the batch being redone), then append every P entry still parked
+// (atomicCAS dedupes repeated entries) to list[cur].
+template <class T, bool kGrid>
+__device__ void merge_parked(const State<T>& s, cg::grid_group& grid, uint32_t cur, uint32_t nclear,
+                             uint64_t tid, uint64_t stride) {
+  auto sync = [&] {
+    if (kGrid) grid.sync();
+    else __syncthreads();
+  };
+  Ctl* ctl = s.ctl;
+  const uint32_t* list = s.list[cur];
+  for (uint64_t i = tid; i < nclear; i += stride) {
+    const uint32_t v = __ldcg(list + i);
+    if (__ldcg(s.fmark + v) == kParked) s.fmark[v] = 0u;
+  }
+  sync();
+  const uint32_t np = *reinterpret_cast<volatile uint32_t*>(&ctl->park_count);
+  for (uint64_t wb = tid & ~uint64_t(31); wb < np; wb += stride) {
+    const uint64_t i = wb + (threadIdx.x & 31);
+    bool keep = false;
+    uint32_t v = 0;
+    if (i < np) {
+      v = __ldcg(s.F + i);
+      keep = __ldcg(s.fmark + v) == kParked && atomicCAS(&s.fmark[v], kParked, 0u) == kParked;
+    }
+    warp_append(keep, v, s.list[cur], &ctl->list_count[cur]);
+  }
+  sync();
+  if (tid == 0) {
+    ctl->park_count = 0;
+    ++ctl->merges;
+  }
+  sync();
+}
+
+// One batch: fix (rule pass, or the FPmin fallback alone when fallback_only),
+// frontier refresh, rebuild.  Parking is on in the rule pass only.
 template <class T, int DIM>
 __device__ BatchResult big_batch(const State<T>& s, cg::grid_group& grid, int kind, uint32_t n,
                                  uint32_t cur, uint32_t it, uint32_t batch_base,
-                                 uint32_t mark_base) {
+                                 uint32_t mark_base, bool fallback_only) {
   Ctl* ctl = s.ctl;
   const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
@@ -1051,13 +1121,17 @@ __device__ BatchResult big_batch(const State<T>& s, cg::grid_group& grid, int ki
   const uint32_t batch = batch_base + 2 * it, mark = mark_base + it;
   uint64_t t0 = 0, t1 = 0, t2 = 0;
   if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  fix_batch(s, s.list[cur], n, rule, batch, &ctl->s_count, tid, stride);
-  grid.sync();
-  uint32_t applied = *reinterpret_cast<volatile uint32_t*>(&ctl->s_count);
+  uint32_t applied = 0;
+  if (!fallback_only) {
+    fix_batch(s, s.list[cur], n, rule, batch, &ctl->s_count, tid, stride, nullptr, nullptr, s.F,
+              &ctl->park_count);
+    grid.sync();
+    applied = *reinterpret_cast<volatile uint32_t*>(&ctl->s_count);
+    if (applied == 0 && kind == 1 && *reinterpret_cast<volatile uint32_t*>(&ctl->park_count))
+      return {kNeedMerge, 0};
+  }
   if (applied == 0 && kind == 1) {
     grid.sync();  // every thread has read applied == 0 before the fallback appends to S
-    if (tid == 0) ctl->retry_count = 0;
-    grid.sync();
     fix_batch(s, s.list[cur], n, 2, batch + 1, &ctl->s_count, tid, stride);
     grid.sync();
     applied = *reinterpret_cast<volatile uint32_t*>(&ctl->s_count);
@@ -1085,7 +1159,6 @@ __device__ BatchResult big_batch(const State<T>& s, cg::grid_group& grid, int ki
     ctl->phase_ns[2] += t3 - t2;
     ctl->s_count = 0;
     ctl->f_count = 0;
-    ctl->retry_count = 0;
     ctl->list_count[cur] = 0;
   }
   return {applied, nf};
@@ -1094,16 +1167,22 @@ __device__ BatchResult big_batch(const State<T>& s, cg::grid_group& grid, int ki
 template <class T, int DIM>
 __device__ BatchResult small_batch(const State<T>& s, int kind, uint32_t n, uint32_t cur,
                                    uint32_t it, uint32_t batch_base, uint32_t mark_base,
-                                   uint32_t* cnt /* smem [4] */) {
+                                   bool fallback_only, uint32_t* cnt /* smem [4] */) {
   const uint64_t tid = threadIdx.x, stride = blockDim.x;
   const int rule = (kind == 0 || kind == 3) ? 0 : 1;
   const uint32_t batch = batch_base + 2 * it, mark = mark_base + it;
-  fix_batch(s, s.list[cur], n, rule, batch, &cnt[0], tid, stride);
-  __syncthreads();
-  uint32_t applied = *reinterpret_cast<volatile uint32_t*>(&cnt[0]);
-  if (applied == 0 && kind == 1) {
+  uint32_t applied = 0;
+  if (!fallback_only) {
+    fix_batch(s, s.list[cur], n, rule, batch, &cnt[0], tid, stride, nullptr, nullptr, s.F,
+              &s.ctl->park_count);
     __syncthreads();
-    if (threadIdx.x == 0) cnt[3] = 0;
+    applied = *reinterpret_cast<volatile uint32_t*>(&cnt[0]);
+    if (applied == 0 && kind == 1 && *reinterpret_cast<volatile uint32_t*>(&s.ctl->park_count)) {
+      __syncthreads();
+      return {kNeedMerge, 0};
+    }
+  }
+  if (applied == 0 && kind == 1) {
     __syncthreads();
     fix_batch(s, s.list[cur], n, 2, batch + 1, &cnt[0], tid, stride);
     __syncthreads();
@@ -1127,7 +1206,7 @@ __device__ BatchResult small_batch(const State<T>& s, int kind, uint32_t n, uint
 template <class T, int DIM>
 __global__ void __launch_bounds__(kSubThreads, 2)
     k_subloop(State<T> s, int kind, uint64_t cap, uint32_t batch_base, uint32_t mark_base,
-              uint32_t max_batches, uint32_t small_max, uint32_t huge_min) {
+              uint32_t max_batches, uint32_t small_max, uint32_t huge_min, uint32_t park_cap) {
   cg::grid_group grid = cg::this_grid();
   Ctl* ctl = s.ctl;
   __shared__ uint32_t cmd[4];
@@ -1135,7 +1214,9 @@ __global__ void __launch_bounds__(kSubThreads, 2)
   if (threadIdx.x < 4) cnt[threadIdx.x] = 0;
   __syncthreads();
 
-  if (blockIdx.x != 0) {  // worker CTAs: join broadcast batches
+  if (blockIdx.x != 0) {  // worker CTAs: join broadcast batches and merges
+    const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     uint32_t seen = 0;
     for (;;) {
       if (threadIdx.x == 0) {
@@ -1152,7 +1233,10 @@ __global__ void __launch_bounds__(kSubThreads, 2)
       const uint32_t type = cmd[0], n = cmd[1], cur = cmd[2], it = cmd[3];
       __syncthreads();
       if (type == kCmdExit) break;
-      big_batch<T, DIM>(s, grid, kind, n, cur, it, batch_base, mark_base);
+      if (type == kCmdMerge)
+        merge_parked<T, true>(s, grid, cur, n, tid, stride);
+      else
+        big_batch<T, DIM>(s, grid, kind, n, cur, it, batch_base, mark_base, type == kCmdFallback);
     }
     grid.sync();
     return;
@@ -1162,8 +1246,33 @@ __global__ void __launch_bounds__(kSubThreads, 2)
   uint64_t attempted = *reinterpret_cast<volatile uint64_t*>(&ctl->attempted);
   uint64_t iters = 0, edits = 0, frontier = 0, big = 0, small_ns = 0, big_ns = 0, items = 0;
   uint32_t status = kStatusOk, done = 0, seq = 0;
+  auto post = [&](uint32_t type, uint32_t n, uint32_t it) {
+    if (threadIdx.x == 0) {
+      ctl->cmd_type = type;
+      ctl->cmd_n = n;
+      ctl->cmd_cur = cur;
+      ctl->cmd_it = it;
+      __threadfence();
+      atomicExch(&ctl->cmd_seq, ++seq);
+    }
+  };
+  // merge P into list[cur]: grid-wide when large, else in this CTA
+  auto merge = [&](uint32_t nclear) {
+    const uint32_t np = *reinterpret_cast<volatile uint32_t*>(&ctl->park_count);
+    if (np + nclear > small_max) {
+      post(kCmdMerge, nclear, 0);
+      merge_parked<T, true>(s, grid, cur, nclear, threadIdx.x, static_cast<uint64_t>(gridDim.x) * blockDim.x);
+    } else {
+      merge_parked<T, false>(s, grid, cur, nclear, threadIdx.x, blockDim.x);
+    }
+  };
   for (;;) {
-    const uint32_t n = *reinterpret_cast<volatile uint32_t*>(&ctl->list_count[cur]);
+    uint32_t n = *reinterpret_cast<volatile uint32_t*>(&ctl->list_count[cur]);
+    const uint32_t np = *reinterpret_cast<volatile uint32_t*>(&ctl->park_count);
+    if (np && (n == 0 || n > huge_min || done >= max_batches || np + n > park_cap)) {
+      merge(0);
+      n = *reinterpret_cast<volatile uint32_t*>(&ctl->list_count[cur]);
+    }
     if (n == 0 || done >= max_batches) break;
     if (n > huge_min) {
       status = kStatusHuge;
@@ -1178,30 +1287,25 @@ __global__ void __launch_bounds__(kSubThreads, 2)
     BatchResult r;
     uint64_t t0 = 0;
     if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    if (n <= small_max) {
-      r = small_batch<T, DIM>(s, kind, n, cur, it, batch_base, mark_base, cnt);
-      if (threadIdx.x == 0) {
-        uint64_t t1;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-        small_ns += t1 - t0;
+    bool fallback_only = false;
+    for (;;) {  // at most twice: the rule pass, then (kNeedMerge) the fallback over list ∪ P
+      if (n <= small_max) {
+        r = small_batch<T, DIM>(s, kind, n, cur, it, batch_base, mark_base, fallback_only, cnt);
+      } else {
+        post(fallback_only ? kCmdFallback : kCmdBatch, n, it);
+        r = big_batch<T, DIM>(s, grid, kind, n, cur, it, batch_base, mark_base, fallback_only);
+        ++big;
+        __syncthreads();
       }
-    } else {
-      if (threadIdx.x == 0) {
-        ctl->cmd_type = kCmdBatch;
-        ctl->cmd_n = n;
-        ctl->cmd_cur = cur;
-        ctl->cmd_it = it;
-        __threadfence();
-        atomicExch(&ctl->cmd_seq, ++seq);
-      }
-      r = big_batch<T, DIM>(s, grid, kind, n, cur, it, batch_base, mark_base);
-      ++big;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        uint64_t t1;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-        big_ns += t1 - t0;
-      }
+      if (r.applied != kNeedMerge) break;
+      merge(n);
+      n = *reinterpret_cast<volatile uint32_t*>(&ctl->list_count[cur]);
+      fallback_only = true;
+    }
+    if (threadIdx.x == 0) {
+      uint64_t t1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      (n <= small_max ? small_ns : big_ns) += t1 - t0;
     }
     if (r.applied == 0) {
       status = kStatusStall;
@@ -1214,11 +1318,9 @@ __global__ void __launch_bounds__(kSubThreads, 2)
     cur ^= 1;
     ++done;
   }
-  if (threadIdx.x == 0) {
-    ctl->cmd_type = kCmdExit;
-    __threadfence();
-    atomicExch(&ctl->cmd_seq, ++seq);
-  }
+  // every exit leaves the complete worklist in list[cur] (huge batches, errors, on_batch)
+  if (*reinterpret_cast<volatile uint32_t*>(&ctl->park_count)) merge(0);
+  post(kCmdExit, 0, 0);
   grid.sync();
   if (threadIdx.x == 0) {
     ctl->cur = cur;
