@@ -173,6 +173,9 @@ CONFIG_CASES = [
     ("trig", [177, 95, 48], 0, 1e-4, np.float32),             # C2 (trig, 1e-4)
     ("gaussian-mixture", [360, 240], 0, 1e-4, np.float32),   # C5 shape, reduced
     ("gaussian-mixture", [48, 40, 24], 2, 1e-3, np.float64),
+    # the bench workload's generator (C4 is 1024^3): big FPmin batches, parked
+    # items and fallbacks inside the persistent subloop
+    ("multi-scale", [96, 96, 48], 0, 1e-3, np.float32),
 ]
 
 
