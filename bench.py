@@ -12,9 +12,12 @@ postconditions → EditSet compaction) over one synthetic field.
            between steps by a 512 MB write outside the events); max over ranks.
 * e2e    — the public host API (derive_edits_into) from pinned host buffers:
            H2D of f and f̂ plus D2H of the EditSet inside the timed region.
-* roofline — the dominant kernel class by device time, from per-launch CUDA
-           events on the engine's stream during the timed steps (profile=1),
-           achieved = algorithmic bytes per launch / mean launch time.
+* roofline — the graded kernel (the streaming class with the most device
+           time, picked from one fully profiled warm-up step), from per-launch
+           CUDA events on the engine's stream during the timed steps (only that
+           class is event-timed there), achieved = algorithmic bytes per launch
+           / mean launch time; per_class and kernel_profile_ms_per_step come
+           from the profiled warm-up step.
 * cpu_baseline — the UNMODIFIED reference (oracle/_ref/libmssz_ref.so,
            OpenMP, all host cores) on a bounded sample of the same workload.
 
@@ -305,10 +308,10 @@ def main():
     d_val = torch.empty(cap, dtype=tdtype, device=dev)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
-    opts = P.DeriveOptions(subloop_cap=cfg.subloop_cap, device=dist.local,
-                           profile=not args.no_profile)
+    opts = P.DeriveOptions(subloop_cap=cfg.subloop_cap, device=dist.local)
 
-    def step():
+    def step(profile=False):
+        opts.profile = profile
         if comm is not None:
             c, _, s = comm.derive_edits_device(dims, df.data_ptr(), dfh.data_ptr(), xi,
                                                d_idx.data_ptr(), d_val.data_ptr(), cap, dtype,
@@ -317,9 +320,24 @@ def main():
         return P.derive_edits_device(topo, df.data_ptr(), dfh.data_ptr(), xi, d_idx.data_ptr(),
                                      d_val.data_ptr(), cap, dtype, opts, stream.cuda_stream)
 
-    for _ in range(args.warmup):
-        count, st = step()
+    # The last warm-up step times every kernel class (CUDA events around each
+    # launch): it gives the per-class breakdown and picks the graded kernel.  The
+    # timed steps then time only that class, so ~10k event records per step do
+    # not inflate the headline; its roofline comes from the timed region.
+    prof_stats = None
+    for w in range(max(args.warmup, 0 if args.no_profile else 1)):
+        last = w == max(args.warmup, 1) - 1
+        count, st = step(profile=last and not args.no_profile)
+        if last and not args.no_profile:
+            prof_stats = st
     torch.cuda.synchronize()
+    top = None
+    if prof_stats is not None:
+        kp = prof_stats.kernel_profile()
+        cand = {k: v["ms"] for k, v in kp.items()
+                if v["launches"] and alg_bytes(k, es, n_local, prof_stats, v["launches"])}
+        top = max(cand, key=cand.get) if cand else None
+    timed_profile = P.profile_mask(top) if top else False
 
     dist.barrier()
     torch.cuda.synchronize()
@@ -330,7 +348,7 @@ def main():
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        count, st = step()
+        count, st = step(profile=timed_profile)
         b.record(stream)
         b.synchronize()
         step_ms.append(a.elapsed_time(b))
@@ -346,28 +364,26 @@ def main():
     peak, peak_src = load_peaks()
     roofline = None
     prof = {}
-    if not args.no_profile:
-        agg = {name: {"launches": 0, "ms": 0.0} for name in P.PROF_CLASSES}
-        for s in stats:
-            for name, d in s.kernel_profile().items():
-                agg[name]["launches"] += d["launches"]
-                agg[name]["ms"] += d["ms"]
-        prof = {k: {"launches": v["launches"] // len(stats), "ms": v["ms"] / len(stats)}
-                for k, v in agg.items() if v["launches"]}
-        tpath = os.path.join(ROOT, "profiles", "ncu_traffic_c4.json")
+    if prof_stats is not None:
+        # per-class breakdown: the fully profiled warm-up step
+        pk = prof_stats.kernel_profile()
+        prof = {k: {"launches": v["launches"], "ms": v["ms"]} for k, v in pk.items() if v["launches"]}
+    if prof_stats is not None and top is not None:
+        total_ms = sum(v["ms"] for v in prof.values())
         graded = {}
-        for k, v in agg.items():
-            if not v["launches"]:
-                continue
-            tot = sum(alg_bytes(k, es, n_local, s, s.kernel_profile()[k]["launches"]) for s in stats)
+        for k, v in prof.items():
+            tot = alg_bytes(k, es, n_local, prof_stats, v["launches"])
             if tot:
                 graded[k] = {"launches": v["launches"], "ms": v["ms"], "bytes": tot,
                              "achieved_GBps": tot / (v["ms"] * 1e-3) / 1e9}
-        top = max(graded, key=lambda k: graded[k]["ms"])
-        per_launch_ms = graded[top]["ms"] / graded[top]["launches"]
-        bytes_per_launch = graded[top]["bytes"] / graded[top]["launches"]
-        achieved = graded[top]["achieved_GBps"]
-        total_ms = sum(v["ms"] for v in agg.values())
+        # the graded kernel: achieved from its launches inside the timed steps
+        t_launch = sum(s.kernel_profile()[top]["launches"] for s in stats)
+        t_ms = sum(s.kernel_profile()[top]["ms"] for s in stats)
+        t_bytes = sum(alg_bytes(top, es, n_local, s, s.kernel_profile()[top]["launches"]) for s in stats)
+        per_launch_ms = t_ms / t_launch
+        bytes_per_launch = t_bytes / t_launch
+        achieved = t_bytes / (t_ms * 1e-3) / 1e9
+        tpath = os.path.join(ROOT, "profiles", "ncu_traffic_c4.json")
         traffic = None  # measured DRAM bytes per launch of this kernel (committed ncu capture, same config)
         if cfg.name == "C4" and dims == cfg.dims and os.path.exists(tpath):
             with open(tpath) as fp:
@@ -375,8 +391,8 @@ def main():
         # the dominant kernel by device time (the persistent C-loop kernel) has no
         # streaming algorithmic byte count: it moves random 32 B sectors; report its
         # measured DRAM throughput (ncu capture of the heaviest launch, same config)
-        dom = max(agg, key=lambda k: agg[k]["ms"])
-        dominant = {"kernel": dom, "share_of_device_time": agg[dom]["ms"] / total_ms if total_ms else None}
+        dom = max(prof, key=lambda k: prof[k]["ms"])
+        dominant = {"kernel": dom, "share_of_device_time": prof[dom]["ms"] / total_ms if total_ms else None}
         if os.path.exists(tpath) and cfg.name == "C4" and dims == cfg.dims:
             with open(tpath) as fp:
                 ent = json.load(fp).get(dom) or {}
@@ -390,10 +406,12 @@ def main():
                     "peak_source": peak_src,
                     "alg_bytes_per_launch": bytes_per_launch,
                     "mean_launch_us": per_launch_ms * 1e3,
-                    "share_of_device_time": graded[top]["ms"] / total_ms if total_ms else None,
+                    "timed_launches": t_launch,
+                    "share_of_device_time": prof[top]["ms"] / total_ms if total_ms else None,
                     "dominant_kernel": dominant,
-                    "per_class": {k: {"launches_per_step": v["launches"] // len(stats),
-                                      "ms_per_step": v["ms"] / len(stats),
+                    "per_class_source": "one fully profiled warm-up step (every launch timed)",
+                    "per_class": {k: {"launches_per_step": v["launches"],
+                                      "ms_per_step": v["ms"],
                                       "achieved_GBps": v["achieved_GBps"],
                                       "frac": v["achieved_GBps"] / peak} for k, v in graded.items()}}
 

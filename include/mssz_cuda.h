@@ -71,7 +71,8 @@ typedef struct mssz_cu_options {
   int32_t device;       /* CUDA ordinal; -1 = current device */
   void (*on_batch)(const void* g_host, uint64_t n, void* user); /* NULL = off */
   void* on_batch_user;
-  int32_t profile; /* 1 = time every kernel with CUDA events (stats.kernel_ms) */
+  int32_t profile; /* CUDA-event kernel timing into stats.kernel_ms: bit 0 = every class,
+                      bit (c + 1) = class c only (MSSZ_CU_PROF_*) */
   int32_t reserved;
 } mssz_cu_options;
 
@@ -121,7 +122,7 @@ typedef struct mssz_cu_stats {
   uint64_t sparse_up;         /* sum of |Up(X)| over sparse passes */
   uint64_t rfix_divergent;    /* (vertex, family) pairs k_rfix_tiles resolved a label for */
   uint64_t kernel_count[MSSZ_CU_PROF_CLASSES]; /* launches per kernel class */
-  double kernel_ms[MSSZ_CU_PROF_CLASSES];      /* device ms per class (profile = 1 only) */
+  double kernel_ms[MSSZ_CU_PROF_CLASSES];      /* device ms per profiled class */
 } mssz_cu_stats;
 
 void mssz_cu_default_options(mssz_cu_options* opt);

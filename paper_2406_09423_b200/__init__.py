@@ -20,7 +20,7 @@ import ctypes as C
 import os
 from dataclasses import dataclass, field
 from enum import IntEnum
-from typing import Callable, Optional
+from typing import Callable, Optional, Union
 
 import numpy as np
 
@@ -34,7 +34,7 @@ __all__ = [
     "detect_kind", "lower_step", "representable_floor", "apply_edits", "segmentation_equal",
     "library", "build", "slab_range", "derive_edits_slabs", "SlabComm",
     "VerificationReport", "build_report", "build_report_device", "segmentation", "export_labels",
-    "compress_base", "decompress_base", "encode_edits",
+    "compress_base", "decompress_base", "encode_edits", "PROF_CLASSES", "profile_mask",
 ]
 
 FPMAX, FPMIN, FNMAX, FNMIN = 0, 1, 2, 3
@@ -123,7 +123,9 @@ class DeriveOptions:
     force: bool = False
     device: int = -1
     on_batch: Optional[Callable[[np.ndarray], None]] = None
-    profile: bool = False  # per-kernel CUDA-event timing into EditStats.kernel_ms
+    # per-kernel CUDA-event timing into EditStats.kernel_ms: True = every class,
+    # or an int mask from profile_mask(...) for selected classes only
+    profile: Union[bool, int] = False
 
 
 @dataclass
@@ -266,6 +268,11 @@ _ARRAY_FIELDS = ("sub_iterations", "kernel_count", "kernel_ms")
 PROF_CLASSES = ["validate", "directions", "detect_kind", "detect_all", "subloop", "label_init",
                 "label_jump", "rfix", "frontier", "compact", "label_finish", "fix", "sparse",
                 "detect_dirty"]
+
+
+def profile_mask(*classes: str) -> int:
+    """DeriveOptions.profile value that times only the named kernel classes."""
+    return sum(1 << (PROF_CLASSES.index(c) + 1) for c in classes)
 
 
 _BATCH_CB = C.CFUNCTYPE(None, C.c_void_p, C.c_uint64, C.c_void_p)

@@ -373,8 +373,10 @@ struct Engine {
 
   // Per-kernel-class device time (CUDA events on the launching stream), only
   // when opt.profile is set: bench.py's roofline reads kernel_ms / kernel_count.
+  // opt.profile: bit 0 = every class, bit (cls + 1) = class cls only
+  bool profiled(int cls) const { return (opt.profile & 1) || ((opt.profile >> (cls + 1)) & 1); }
   void pre(int cls) {
-    if (!opt.profile) return;
+    if (!profiled(cls)) return;
     ws.prof_ev(prof_n * 2);
     CK(cudaEventRecord(ws.pev[prof_n * 2], ws.stream));
     prof_cls.push_back(cls);
@@ -384,7 +386,7 @@ struct Engine {
     ++st.kernel_launches;
     ++st.kernel_count[cls];
     CK_LAUNCH();
-    if (!opt.profile) return;
+    if (!profiled(cls)) return;
     CK(cudaEventRecord(ws.pev[prof_n * 2 + 1], ws.stream));
     ++prof_n;
   }

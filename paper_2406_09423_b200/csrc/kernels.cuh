@@ -831,14 +831,25 @@ __device__ __forceinline__ void frontier_update(const State<T>& s, uint32_t ns, 
   __shared__ uint32_t nstage[kStageWarps][kStageK * 32];
   WarpBuffer<kStageK> nbuf(warp_stage(nstage));
   uint32_t nmine = 0;
+  // software pipeline: each lane's edited vertex is loaded one iteration ahead
+  // (it heads the dependent chain S -> gdir -> g -> fmark -> recompute)
+  uint32_t sv_next = 0;
+  {
+    const uint64_t i0 = (tid & ~uint64_t(31)) + (threadIdx.x & 31);
+    if (i0 < total && static_cast<int>(i0 % LPS) <= NS) sv_next = __ldcg(s.S + i0 / LPS);
+  }
   for (uint64_t wb = tid & ~uint64_t(31); wb < total; wb += stride) {
     const uint64_t i = wb + (threadIdx.x & 31);
+    const uint32_t sv = sv_next;
+    {
+      const uint64_t in = i + stride;
+      if (in < total && static_cast<int>(in % LPS) <= NS) sv_next = __ldcg(s.S + in / LPS);
+    }
     bool mine = false, keep = false;
     uint32_t u = 0;
     if (i < total) {
       const int k = static_cast<int>(i % LPS) - 1;  // -1 = the edited vertex itself
       if (k < NS) {
-        const uint32_t sv = __ldcg(s.S + i / LPS);
         uint32_t x, y, z;
         coords(s.geo, sv, x, y, z);
         int dx = 0, dy = 0, dz = 0;
@@ -859,7 +870,8 @@ __device__ __forceinline__ void frontier_update(const State<T>& s, uint32_t ns, 
             const uint8_t code =
                 static_cast<uint8_t>(direction_code<T, DIM, true>(s.g, s.geo, u, ux, uy, uz));
             if (next) keep = kind_match(kind, __ldg(s.fdir + u), code);
-            if (s.gdir[u] != code) {
+            // cu is u's pre-batch code: only the fmark winner writes gdir[u]
+            if (cu != code) {
               s.gdir[u] = code;
               if (s.cstamp && s.cstamp[u >> 6] != mark) s.cstamp[u >> 6] = mark;
               if (s.tdirty) s.tdirty[label_tile_of<DIM>(s.geo, ux, uy, uz)] = 1;

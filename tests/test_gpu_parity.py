@@ -281,3 +281,22 @@ def test_device_entry_point_matches_host(P):
     assert dv[:count].cpu().numpy().tobytes() == host.values.tobytes()
     # fhat on the device is untouched (the engine edits its own copy)
     assert dfh.cpu().numpy().tobytes() == fh.tobytes()
+
+
+def test_profile_class_mask(P):
+    """DeriveOptions.profile: True times every class, profile_mask(...) only the named ones."""
+    from paper_2406_09423_b200 import inputs as I
+    dims = [64, 48, 24]
+    f = I.generate("random-smooth", dims, 1, np.float32)
+    xi = I.resolve_rel(f, 1e-3)
+    fh = I.compress_base(dims, f, xi)
+    topo = P.build_topology(dims)
+    full, only = P.EditStats(), P.EditStats()
+    a = P.derive_edits(topo, f, fh, xi, P.DeriveOptions(profile=True), full)
+    b = P.derive_edits(topo, f, fh, xi, P.DeriveOptions(profile=P.profile_mask("directions")), only)
+    assert np.array_equal(a.indices, b.indices) and a.values.tobytes() == b.values.tobytes()
+    kf, ko = full.kernel_profile(), only.kernel_profile()
+    assert sum(1 for v in kf.values() if v["ms"] > 0) >= 3
+    assert ko["directions"]["ms"] > 0
+    assert all(v["ms"] == 0 for k, v in ko.items() if k != "directions")
+    assert ko["directions"]["launches"] == kf["directions"]["launches"]
