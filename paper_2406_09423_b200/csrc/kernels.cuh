@@ -831,55 +831,61 @@ __device__ __forceinline__ void frontier_update(const State<T>& s, uint32_t ns, 
   __shared__ uint32_t nstage[kStageWarps][kStageK * 32];
   WarpBuffer<kStageK> nbuf(warp_stage(nstage));
   uint32_t nmine = 0;
-  // software pipeline: each lane's edited vertex is loaded one iteration ahead
-  // (it heads the dependent chain S -> gdir -> g -> fmark -> recompute)
-  uint32_t sv_next = 0;
-  {
-    const uint64_t i0 = (tid & ~uint64_t(31)) + (threadIdx.x & 31);
-    if (i0 < total && static_cast<int>(i0 % LPS) <= NS) sv_next = __ldcg(s.S + i0 / LPS);
-  }
+  // software pipeline over the dependent chain S -> gdir -> g -> fmark ->
+  // recompute: a lane's edited vertex is loaded two iterations ahead and its
+  // neighbour's code one iteration ahead
+  constexpr uint32_t kNone = 0xFFFFFFFFu;
+  auto load_sv = [&](uint64_t i) -> uint32_t {
+    return (i < total && static_cast<int>(i % LPS) <= NS) ? __ldcg(s.S + i / LPS) : 0u;
+  };
+  auto locate = [&](uint64_t i, uint32_t sv) -> uint32_t {  // lane i's vertex u, or kNone
+    if (i >= total) return kNone;
+    const int k = static_cast<int>(i % LPS) - 1;  // -1 = the edited vertex itself
+    if (k >= NS) return kNone;
+    uint32_t x, y, z;
+    coords(s.geo, sv, x, y, z);
+    int dx = 0, dy = 0, dz = 0;
+    if (k >= 0) slot_delta<DIM>(k, dx, dy, dz);
+    const uint32_t ux = x + dx, uy = y + dy, uz = z + dz;
+    if (!(ux < s.geo.X && uy < s.geo.Y && (DIM == 2 || uz < s.geo.Z))) return kNone;
+    const uint32_t u = ux + s.geo.X * uy + s.geo.XY * uz;
+    return u - s.act_lo < s.act_n ? u : kNone;
+  };
+  const uint64_t i0 = (tid & ~uint64_t(31)) + (threadIdx.x & 31);
+  uint32_t sv_c = load_sv(i0), sv_n = load_sv(i0 + stride);
+  uint32_t u_c = locate(i0, sv_c);
+  uint32_t cu_c = u_c != kNone ? __ldcg(s.gdir + u_c) : 0u;
   for (uint64_t wb = tid & ~uint64_t(31); wb < total; wb += stride) {
     const uint64_t i = wb + (threadIdx.x & 31);
-    const uint32_t sv = sv_next;
-    {
-      const uint64_t in = i + stride;
-      if (in < total && static_cast<int>(in % LPS) <= NS) sv_next = __ldcg(s.S + in / LPS);
-    }
+    const uint32_t sv_nn = load_sv(i + 2 * stride);
+    const uint32_t u_n = locate(i + stride, sv_n);
+    const uint32_t cu_n = u_n != kNone ? __ldcg(s.gdir + u_n) : 0u;
     bool mine = false, keep = false;
-    uint32_t u = 0;
-    if (i < total) {
-      const int k = static_cast<int>(i % LPS) - 1;  // -1 = the edited vertex itself
-      if (k < NS) {
-        uint32_t x, y, z;
-        coords(s.geo, sv, x, y, z);
-        int dx = 0, dy = 0, dz = 0;
-        if (k >= 0) slot_delta<DIM>(k, dx, dy, dz);
-        const uint32_t ux = x + dx, uy = y + dy, uz = z + dz;
-        if (ux < s.geo.X && uy < s.geo.Y && (DIM == 2 || uz < s.geo.Z) &&
-            (u = ux + s.geo.X * uy + s.geo.XY * uz) - s.act_lo < s.act_n) {
-          const uint32_t cu = __ldcg(s.gdir + u);
-          const uint32_t ca = cu & 15u, cd = cu >> 4;
-          const uint32_t um = cd == kSelf ? u : u + s.geo.off[cd];
-          bool fire = (ca == kSelf ? u : u + s.geo.off[ca]) == sv;
-          if (!fire && um != sv) {
-            const auto kt = okey(__ldcg(s.g + sv)), km = okey(__ldcg(s.g + um));
-            fire = kt < km || (kt == km && sv < um);
-          }
-          if (fire && __ldcg(s.fmark + u) != mark && atomicExch(&s.fmark[u], mark) != mark) {
-            mine = true;
-            const uint8_t code =
-                static_cast<uint8_t>(direction_code<T, DIM, true>(s.g, s.geo, u, ux, uy, uz));
-            if (next) keep = kind_match(kind, __ldg(s.fdir + u), code);
-            // cu is u's pre-batch code: only the fmark winner writes gdir[u]
-            if (cu != code) {
-              s.gdir[u] = code;
-              if (s.cstamp && s.cstamp[u >> 6] != mark) s.cstamp[u >> 6] = mark;
-              if (s.tdirty) s.tdirty[label_tile_of<DIM>(s.geo, ux, uy, uz)] = 1;
-              if (s.cdirty) {  // test first: neighbouring edits share the chunk bit
-                const uint32_t bit = 1u << ((u >> 6) & 31);
-                if (!(s.cdirty[u >> 11] & bit)) atomicOr(&s.cdirty[u >> 11], bit);
-              }
-            }
+    const uint32_t u = u_c == kNone ? 0u : u_c;
+    if (u_c != kNone) {
+      const uint32_t sv = sv_c, cu = cu_c;
+      const uint32_t ca = cu & 15u, cd = cu >> 4;
+      const uint32_t um = cd == kSelf ? u : u + s.geo.off[cd];
+      bool fire = (ca == kSelf ? u : u + s.geo.off[ca]) == sv;
+      if (!fire && um != sv) {
+        const auto kt = okey(__ldcg(s.g + sv)), km = okey(__ldcg(s.g + um));
+        fire = kt < km || (kt == km && sv < um);
+      }
+      if (fire && __ldcg(s.fmark + u) != mark && atomicExch(&s.fmark[u], mark) != mark) {
+        mine = true;
+        uint32_t ux, uy, uz;
+        coords(s.geo, u, ux, uy, uz);
+        const uint8_t code =
+            static_cast<uint8_t>(direction_code<T, DIM, true>(s.g, s.geo, u, ux, uy, uz));
+        if (next) keep = kind_match(kind, __ldg(s.fdir + u), code);
+        // cu is u's pre-batch code: only the fmark winner writes gdir[u]
+        if (cu != code) {
+          s.gdir[u] = code;
+          if (s.cstamp && s.cstamp[u >> 6] != mark) s.cstamp[u >> 6] = mark;
+          if (s.tdirty) s.tdirty[label_tile_of<DIM>(s.geo, ux, uy, uz)] = 1;
+          if (s.cdirty) {  // test first: neighbouring edits share the chunk bit
+            const uint32_t bit = 1u << ((u >> 6) & 31);
+            if (!(s.cdirty[u >> 11] & bit)) atomicOr(&s.cdirty[u >> 11], bit);
           }
         }
       }
@@ -890,6 +896,10 @@ __device__ __forceinline__ void frontier_update(const State<T>& s, uint32_t ns, 
     } else {
       warp_append(mine, u, s.F, f_count);
     }
+    sv_c = sv_n;
+    sv_n = sv_nn;
+    u_c = u_n;
+    cu_c = cu_n;
   }
   if (next) {
     nbuf.flush(next, next_count);
