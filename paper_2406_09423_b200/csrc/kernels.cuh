@@ -1635,9 +1635,19 @@ __global__ void __launch_bounds__(256) k_exit_reset(TileStore ts, const uint32_t
     const size_t o = (static_cast<size_t>(b) * 2 + fam) * ts.surface;
     uint32_t* fin = fam ? finm : finM;
     const uint32_t* prov = fam ? m : M;
-    for (uint32_t k = threadIdx.x; k < n; k += blockDim.x) {
-      const uint32_t e = ts.E[o + k];
-      fin[e] = prov[e];
+    // four exits per thread per step: their loads and gathers overlap
+    for (uint32_t k0 = threadIdx.x; k0 < n; k0 += 4 * blockDim.x) {
+      uint32_t e[4], p[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t k = k0 + q * blockDim.x;
+        e[q] = k < n ? ts.E[o + k] : kNoTarget;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) p[q] = e[q] != kNoTarget ? __ldg(prov + e[q]) : 0u;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (e[q] != kNoTarget) fin[e[q]] = p[q];
     }
   }
 }
@@ -1654,21 +1664,31 @@ __global__ void __launch_bounds__(256) k_exit_jump_tiles(TileStore ts, uint32_t*
     const uint32_t n = ts.Ecnt[b * 2 + fam];
     const size_t o = (static_cast<size_t>(b) * 2 + fam) * ts.surface;
     uint32_t* fin = fam ? finm : finM;
-    for (uint32_t kb = 0; kb < n; kb += blockDim.x) {  // block-uniform (block_reserve)
-      const uint32_t k = kb + threadIdx.x;
-      bool keep = false;
-      uint32_t e = 0;
-      if (k < n) {
-        e = ts.E[o + k];
-        const uint32_t l = fin[e];
-        const uint32_t ll = fin[l];
-        if (ll != l) {
-          fin[e] = ll;
-          keep = fin[ll] != ll;
-        }
+    // block-uniform trip count (block_reserve); two exits per thread per step
+    // so the two 3-deep gather chains overlap
+    for (uint32_t kb = 0; kb < n; kb += 2 * blockDim.x) {
+      uint32_t e[2], l[2], ll[2];
+      bool live[2], keep[2] = {false, false};
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const uint32_t k = kb + threadIdx.x + q * blockDim.x;
+        live[q] = k < n;
+        e[q] = live[q] ? ts.E[o + k] : 0u;
       }
-      const uint32_t pos = block_reserve(keep ? 1u : 0u, cnt_out + fam);  // one atomic per block step
-      if (keep) (fam ? out_d : out_a)[pos] = e;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) l[q] = live[q] ? fin[e[q]] : 0u;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) ll[q] = live[q] ? fin[l[q]] : 0u;
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+        if (live[q] && ll[q] != l[q]) {
+          fin[e[q]] = ll[q];
+          keep[q] = fin[ll[q]] != ll[q];
+        }
+      uint32_t pos = block_reserve((keep[0] ? 1u : 0u) + (keep[1] ? 1u : 0u), cnt_out + fam);
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+        if (keep[q]) (fam ? out_d : out_a)[pos++] = e[q];
     }
   }
 }
