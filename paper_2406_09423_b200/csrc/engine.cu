@@ -158,6 +158,7 @@ struct Workspace {
   Ctl* ctl = nullptr;
   Ctl* hctl = nullptr;  // pinned mirror
   uint32_t next_batch = 1, next_mark = 1;
+  bool fmark_parked = false;  // a sharded C loop raised with parked items: fmark holds kParked
   cudaEvent_t ev[4] = {};
   std::vector<cudaEvent_t> pev;  // profiling event pool
   std::mutex mu;
@@ -227,7 +228,8 @@ struct Workspace {
     fresh |= cstamp.ensure((n + 63) / 64 * 4 + 4);
     lists.ensure(np * 16);  // list0 list1 S F (u32); reused as the u64+T EditSet
     tiles.ensure(((n + kCompactTile - 1) / kCompactTile + 1) * 4);
-    if (fresh || next_batch > 0xF0000000u || next_mark > 0xF0000000u) {
+    if (fresh || fmark_parked || next_batch > 0xF0000000u || next_mark > 0xF0000000u) {
+      fmark_parked = false;
       CK(cudaMemsetAsync(stamp.p, 0, stamp.cap, stream));
       CK(cudaMemsetAsync(fmark.p, 0, fmark.cap, stream));
       CK(cudaMemsetAsync(cstamp.p, 0, cstamp.cap, stream));

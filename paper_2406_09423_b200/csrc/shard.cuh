@@ -65,6 +65,7 @@ struct alignas(8) Rec {
   uint64_t nonfinite;
   uint64_t violations;
   uint64_t err;       // label-table resolution hit a cycle
+  uint64_t parked;    // C loop: parked worklist items (see k_subloop)
 };
 
 __global__ void k_rec(const Ctl* __restrict__ ctl, uint32_t cur, const uint32_t* __restrict__ err,
@@ -81,6 +82,7 @@ __global__ void k_rec(const Ctl* __restrict__ ctl, uint32_t cur, const uint32_t*
   r.nonfinite = ctl->nonfinite;
   r.violations = ctl->violations;
   r.err = *err;
+  r.parked = ctl->park_count;
   *out = r;
 }
 
@@ -88,10 +90,42 @@ __global__ void k_rec(const Ctl* __restrict__ ctl, uint32_t cur, const uint32_t*
 template <class T>
 __global__ void __launch_bounds__(256) k_slab_fix(State<T> s, const uint32_t* __restrict__ list,
                                                   const uint32_t* count, int rule, uint32_t batch,
-                                                  uint32_t* retry, uint32_t* retry_count) {
+                                                  uint32_t* retry, uint32_t* retry_count, bool park) {
   fix_batch(s, list, *count, rule, batch, &s.ctl->s_count,
             static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x,
-            static_cast<uint64_t>(gridDim.x) * blockDim.x, retry, retry_count);
+            static_cast<uint64_t>(gridDim.x) * blockDim.x, retry, retry_count, park ? s.F : nullptr,
+            park ? &s.ctl->park_count : nullptr);
+}
+
+// Parked items (see k_subloop) of the host-driven C loop.  k_unpark_list clears
+// the flag of the worklist items parked by the batch being redone;
+// k_unpark_merge appends every still-parked P entry to the worklist (append =
+// false: only clears the flags, after a streaming refresh rebuilt the list).
+__global__ void __launch_bounds__(256) k_unpark_list(const uint32_t* __restrict__ list, const uint32_t* count,
+                                                     uint32_t* __restrict__ fmark) {
+  const uint32_t n = *count;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t v = list[i];
+    if (__ldcg(fmark + v) == kParked) fmark[v] = 0u;
+  }
+}
+__global__ void __launch_bounds__(256) k_unpark_merge(const uint32_t* __restrict__ P, const uint32_t* np_ptr,
+                                                      uint32_t* __restrict__ fmark, uint32_t* list,
+                                                      uint32_t* count, bool append) {
+  const uint32_t np = *np_ptr;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t wb = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) & ~uint64_t(31); wb < np;
+       wb += stride) {
+    const uint64_t i = wb + (threadIdx.x & 31);
+    bool keep = false;
+    uint32_t v = 0;
+    if (i < np) {
+      v = __ldcg(P + i);
+      keep = __ldcg(fmark + v) == kParked && atomicCAS(&fmark[v], kParked, 0u) == kParked;
+    }
+    if (append) warp_append(keep, v, list, count);
+  }
 }
 
 // Owned targets lowered in this batch that lie on the first / last two owned
@@ -736,16 +770,21 @@ struct SlabEngine {
       const uint32_t it = static_cast<uint32_t>(attempted + 1);
       const uint32_t batch = batch_base + 2 * it, mark = mark_base + it;
       // the fix runs before the global emptiness test: when every list is
-      // empty it is a no-op, and the test then costs no extra round trip
-      fix(rule, batch, S.list[cur], &ws.ctl->list_count[cur], false);
+      // empty it is a no-op, and the test then costs no extra round trip.
+      // Items whose claimed target sits at its floor are parked (k_subloop):
+      // the worklist is the active list plus the parked list P.
+      fix(rule, batch, S.list[cur], &ws.ctl->list_count[cur], false, /*park=*/true);
+      ws.fmark_parked = true;
       gather();
-      const uint64_t total = sum([](const Rec& r) { return r.list; });
+      const uint64_t parked = sum([](const Rec& r) { return r.parked; });
+      const uint64_t total = sum([](const Rec& r) { return r.list; }) + parked;
       if (total == 0) break;
       ++attempted;
       if (attempted > eng.opt.subloop_cap)
         fail(MSSZ_CU_ERR_NON_CONVERGENCE, "%s subloop exceeded its iteration cap", kKindName[kind]);
       uint64_t applied = sum([](const Rec& r) { return r.applied; });
-      if (applied == 0 && kind == 1) {  // FPmin fallback (edit_engine.cpp:262-268)
+      if (applied == 0 && kind == 1) {  // FPmin fallback (edit_engine.cpp:262-268) over list ∪ P
+        if (parked) unpark(cur, /*append=*/true);
         fix(2, batch + 1, S.list[cur], &ws.ctl->list_count[cur], false);
         gather();
         applied = sum([](const Rec& r) { return r.applied; });
@@ -757,6 +796,7 @@ struct SlabEngine {
       CK(cudaMemsetAsync(&ws.ctl->list_count[cur ^ 1], 0, sizeof(uint32_t), ws.stream));
       CK(cudaMemsetAsync(&ws.ctl->f_count, 0, sizeof(uint32_t), ws.stream));
       if (total > n_glob / kHugeBatchDivisor) {  // one streaming sweep beats ~15 RMWs per edit
+        unpark(cur, /*append=*/false);  // the detect below rebuilds the whole list
         eng.directions(S.g, S.gdir);
         detect(kind, S.list[cur ^ 1], &ws.ctl->list_count[cur ^ 1]);
         ++st().huge_batches;
@@ -775,20 +815,34 @@ struct SlabEngine {
       ++iters;
       edits += applied;
     }
+    ws.fmark_parked = false;  // the loop ends with list ∪ P empty
     st().sub_iterations[kind] += iters;
     st().effective_edits += edits;
     return edits;
   }
 
+  // merge P back into list[cur] (append) or only clear its flags; P is emptied
+  void unpark(uint32_t cur, bool append) {
+    State<T>& S = s();
+    if (append)
+      k_unpark_list<<<2 * ws.sms, 256, 0, ws.stream>>>(S.list[cur], &ws.ctl->list_count[cur], S.fmark);
+    k_unpark_merge<<<2 * ws.sms, 256, 0, ws.stream>>>(S.F, &ws.ctl->park_count, S.fmark, S.list[cur],
+                                                      &ws.ctl->list_count[cur], append);
+    CK_LAUNCH();
+    CK(cudaMemsetAsync(&ws.ctl->park_count, 0, sizeof(uint32_t), ws.stream));
+  }
+
   // one fix over a device-counted list; resets the batch counters first
-  void fix(int rule, uint32_t batch, const uint32_t* list, const uint32_t* count, bool retry) {
+  void fix(int rule, uint32_t batch, const uint32_t* list, const uint32_t* count, bool retry,
+           bool park = false) {
     CK(cudaMemsetAsync(&ws.ctl->s_count, 0, sizeof(uint32_t) * 2, ws.stream));  // s_count, f_count
     CK(cudaMemsetAsync(&ws.ctl->retry_count, 0, sizeof(uint32_t), ws.stream));
     eng.pre(kProfFix);
     // grid-stride over a device-side count: 2 CTAs per SM whatever the batch size
     k_slab_fix<T><<<2 * ws.sms, 256, 0, ws.stream>>>(s(), list, count, rule, batch,
                                                                    retry ? s().F : nullptr,
-                                                                   retry ? &ws.ctl->retry_count : nullptr);
+                                                                   retry ? &ws.ctl->retry_count : nullptr,
+                                                                   park);
     eng.launched(kProfFix);
     pack();
   }
