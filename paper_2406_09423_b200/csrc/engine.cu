@@ -335,6 +335,12 @@ struct Engine {
   // a full direction sweep invalidates that (fresh[k] = false)
   uint32_t end_mark[4] = {0, 0, 0, 0};
   bool fresh[4] = {false, false, false, false};
+  // code_epoch advances whenever g-codes may have changed (a subloop or R loop
+  // with edits, a full sweep); a fresh kind whose list ran empty at epoch
+  // epoch_end[k] still has an empty list while the epoch is unchanged, so its
+  // subloop is skipped without a launch (no chunk can be stamped since)
+  uint64_t code_epoch = 1;
+  uint64_t epoch_end[4] = {0, 0, 0, 0};
   float dir_ms = 0.f, lab_ms = 0.f;
   SlabRes sres{};  // z-slab label resolution for k_rfix_tiles (tab == nullptr: single device)
 
@@ -408,8 +414,10 @@ struct Engine {
   void directions(const T* vals, uint8_t* dir) {
     if (dir == s.gdir && s.cdirty)  // every code may change: X must re-evaluate all chunks
       CK(cudaMemsetAsync(s.cdirty, 0xFF, (n() + 2047) / 2048 * 4, ws.stream));
-    if (dir == s.gdir)
+    if (dir == s.gdir) {
       for (bool& f : fresh) f = false;
+      ++code_epoch;
+    }
     pre(kProfDirections);
     const uint64_t want = static_cast<uint64_t>(ws.sms) * 8;
     if (geo.ndims == 2) {
@@ -717,6 +725,7 @@ struct Engine {
 
   // run_subloop (edit_engine.cpp:246-278)
   uint64_t run_subloop(int kind) {
+    if (fresh[kind] && epoch_end[kind] == code_epoch && !opt.on_batch) return 0;  // list provably empty
     reset_ctl();
     ws.push_ctl();
     const int dcls = fresh[kind] ? kProfDetectDirty : kProfDetectKind;
@@ -788,6 +797,7 @@ struct Engine {
     st.effective_edits += c.edits;
     st.frontier_vertices += c.frontier;
     st.big_batches += c.big_batches;
+    if (c.edits) ++code_epoch;
     return c.edits;
   }
 
@@ -800,6 +810,7 @@ struct Engine {
         pass_edits += run_subloop(kind);
         end_mark[kind] = ws.next_mark;  // every later batch uses marks >= this
         fresh[kind] = true;
+        epoch_end[kind] = code_epoch;
       }
       if (pass_edits) r_full_valid = false;  // the tile store no longer matches gdir
       if (pass_edits == 0) return;
@@ -960,6 +971,7 @@ struct Engine {
   // codes changed are re-resolved, and only tiles that are dirty or whose exits
   // changed their final label recompute their mismatch bits.
   bool run_r_loop() {
+    ++code_epoch;  // conservatively: R batches refresh codes
     uint64_t iters = 0;
     bool first = true;
     TileStore ts = tile_store();
