@@ -750,6 +750,9 @@ struct SlabEngine {
 
   // ---- run_subloop (edit_engine.cpp:246-278), one host-driven batch at a time ----
   uint64_t run_subloop(int kind) {
+    // provably empty on every rank (Engine::run_subloop): edit totals, hence
+    // the epoch, are global
+    if (eng.fresh[kind] && eng.epoch_end[kind] == eng.code_epoch && !eng.opt.on_batch) return 0;
     State<T>& S = s();
     uint32_t& cur = eng.cur;
     reset_ctl();
@@ -818,6 +821,7 @@ struct SlabEngine {
     ws.fmark_parked = false;  // the loop ends with list ∪ P empty
     st().sub_iterations[kind] += iters;
     st().effective_edits += edits;
+    if (edits) ++eng.code_epoch;
     return edits;
   }
 
@@ -855,6 +859,7 @@ struct SlabEngine {
         pass_edits += run_subloop(kind);
         eng.end_mark[kind] = ws.next_mark;  // every later batch uses marks >= this
         eng.fresh[kind] = true;
+        eng.epoch_end[kind] = eng.code_epoch;
       }
       if (pass_edits) r_full_valid = false;  // the C loop does not track dirty label tiles
       if (pass_edits == 0) return;
@@ -918,6 +923,7 @@ struct SlabEngine {
 
   // run_r_loop (edit_engine.cpp:329-366)
   bool run_r_loop() {
+    ++eng.code_epoch;  // conservatively: R batches refresh codes
     uint64_t iters = 0;
     bool first = true, last_frontier = false;
     TileStore ts = eng.tile_store();
