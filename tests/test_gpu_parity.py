@@ -214,6 +214,26 @@ def test_on_batch_snapshots_match_oracle(P, oracle_lib):
         prev = got
 
 
+def test_on_batch_snapshots_multiscale_3d(P, oracle_lib):
+    """Per-batch g on a 3D multi-scale field (FPmin-heavy: parked items are merged
+    back on every kernel exit in on_batch mode, and before each fallback)."""
+    from paper_2406_09423_b200 import inputs as I
+    dims = [24, 20, 12]
+    f = I.generate("multi-scale", dims, 3, np.float32)
+    xi = I.resolve_rel(f, 1e-3)
+    fh = I.compress_base(dims, f, xi)
+    topo = P.build_topology(dims)
+    snaps = []
+    st = P.EditStats()
+    P.derive_edits(topo, f, fh, xi, P.DeriveOptions(on_batch=snaps.append, subloop_cap=100000), st)
+    jac = oracle_lib.derive_edits(dims, f, fh, xi, subloop_cap=100000, schedule=O.JACOBI,
+                                  record_batches=True)
+    assert st.sub_iterations[1] > 0
+    assert len(snaps) == len(jac.batches) > 0
+    for got, want in zip(snaps, jac.batches):
+        assert got.tobytes() == want.tobytes()
+
+
 def test_derive_identity_and_errors(P):
     from paper_2406_09423_b200 import inputs as I
     dims = [12, 12]
