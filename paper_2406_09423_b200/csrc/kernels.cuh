@@ -1454,8 +1454,6 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
   __shared__ int32_t sloc[16];
   __shared__ uint32_t sface[16];
   __shared__ int32_t shalo[16];  // offset in the tile's halo box (exit dedupe bitmap)
-  constexpr int NROW = TL::TY * TL::TZ;  // tile rows (x runs)
-  __shared__ uint32_t rowbase[NROW];     // global id of each row's first vertex
   if (threadIdx.x < 16) {
     int dx = 0, dy = 0, dz = 0;
 #pragma unroll
@@ -1476,8 +1474,6 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
   const int ey = min(TL::TY, static_cast<int>(g.Y - y0));
   const int ez = DIM == 2 ? 1 : min(TL::TZ, static_cast<int>(g.Z - z0));
   const uint32_t base = x0 + g.X * y0 + g.XY * z0;
-  for (int r = threadIdx.x; r < NROW; r += kLabelTileThreads)
-    rowbase[r] = base + g.X * (r & (TL::TY - 1)) + g.XY * (r / TL::TY);
   const bool full = ex == TL::TX && ey == TL::TY && ez == TL::TZ;
   // dir tile: 16-byte vector loads when rows are 16-byte aligned and whole
   if (full && (g.X % 16) == 0) {
@@ -1546,12 +1542,13 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
     const int lx = i & (TL::TX - 1), ly = (i >> TL::LX) & (TL::TY - 1), lz = i >> (TL::LX + TL::LY);
     if (lx < ex && ly < ey && lz < ez) {
       const uint32_t p = own[j];
-      const uint32_t gi = rowbase[i >> TL::LX] + lx;
+      const uint32_t gi = base + lx + g.X * ly + g.XY * lz;
 #pragma unroll
       for (int fam = 0; fam < 2; ++fam) {
         const int t = fam ? (p >> 16) : (p & 0xFFFFu);
         const uint32_t c = (sdir[t] >> (4 * fam)) & 15u;
-        const uint32_t res = rowbase[t >> TL::LX] + (t & (TL::TX - 1)) + soff[c];
+        const uint32_t res = base + (t & (TL::TX - 1)) + g.X * ((t >> TL::LX) & (TL::TY - 1)) +
+                             g.XY * (t >> (TL::LX + TL::LY)) + soff[c];
         (fam ? m : M)[gi] = res;
         // fin is only ever read at provisional-label values: roots (here) and
         // exits (seeded by k_exit_reset), so non-roots need no fin write
@@ -1588,7 +1585,7 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
       const uint32_t code = sdir[i];
       const uint32_t on = (lx == 0 ? 1u : 0u) | (lx == ex - 1 ? 2u : 0u) | (ly == 0 ? 4u : 0u) |
                           (ly == ey - 1 ? 8u : 0u) | (lz == 0 ? 16u : 0u) | (lz == ez - 1 ? 32u : 0u);
-      const uint32_t gi = rowbase[i >> TL::LX] + lx;
+      const uint32_t gi = base + lx + g.X * ly + g.XY * lz;
       const int hb = (lx + 1) + (TL::TX + 2) * ((ly + 1) + (TL::TY + 2) * (DIM == 2 ? 0 : lz + 1));
 #pragma unroll
       for (int fam = 0; fam < 2; ++fam) {
