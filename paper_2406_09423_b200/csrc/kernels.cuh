@@ -1448,10 +1448,9 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
   for (int w = threadIdx.x; w < 2 * ((HBOX + 31) / 32); w += kLabelTileThreads)
     (&seen[0][0])[w] = 0u;
   if (threadIdx.x < 2) sexit_n[threadIdx.x] = 0;
-  // per slot: global offset, local (in-tile) offset, faces of the tile it crosses
+  // per slot: global offset, faces of the tile it crosses
   // (bit 0 -x, 1 +x, 2 -y, 3 +y, 4 -z, 5 +z); SELF = slot 15: offset 0, no face
   __shared__ int32_t soff[16];
-  __shared__ int32_t sloc[16];
   __shared__ uint32_t sface[16];
   __shared__ int32_t shalo[16];  // offset in the tile's halo box (exit dedupe bitmap)
   if (threadIdx.x < 16) {
@@ -1460,10 +1459,29 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
     for (int k = 0; k < NS; ++k)
       if (k == static_cast<int>(threadIdx.x)) stencil<DIM>(k, dx, dy, dz);
     soff[threadIdx.x] = g.off[threadIdx.x];
-    sloc[threadIdx.x] = dx + (dy << TL::LX) + (dz << (TL::LX + TL::LY));
     sface[threadIdx.x] = (dx < 0 ? 1u : 0u) | (dx > 0 ? 2u : 0u) | (dy < 0 ? 4u : 0u) | (dy > 0 ? 8u : 0u) |
                          (dz < 0 ? 16u : 0u) | (dz > 0 ? 32u : 0u);
     shalo[threadIdx.x] = dx + (TL::TX + 2) * (dy + (TL::TY + 2) * dz);
+  }
+  // per direction byte (asc | desc << 4): both local parent offsets (int16 each)
+  // and both face masks, so a local parent costs one shared load
+  __shared__ uint2 scode[256];
+  if (threadIdx.x < 256) {
+    const int ca = threadIdx.x & 15, cd = threadIdx.x >> 4;
+    int ax = 0, ay = 0, az = 0, bx = 0, by = 0, bz = 0;
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      if (k == ca) stencil<DIM>(k, ax, ay, az);
+      if (k == cd) stencil<DIM>(k, bx, by, bz);
+    }
+    const int la = ax + (ay << TL::LX) + (az << (TL::LX + TL::LY));
+    const int lb = bx + (by << TL::LX) + (bz << (TL::LX + TL::LY));
+    auto faces = [](int x, int y, int z) {
+      return (x < 0 ? 1u : 0u) | (x > 0 ? 2u : 0u) | (y < 0 ? 4u : 0u) | (y > 0 ? 8u : 0u) |
+             (z < 0 ? 16u : 0u) | (z > 0 ? 32u : 0u);
+    };
+    scode[threadIdx.x] = make_uint2((static_cast<uint32_t>(la) & 0xFFFFu) | (static_cast<uint32_t>(lb) << 16),
+                                    faces(ax, ay, az) | (faces(bx, by, bz) << 8));
   }
   const uint32_t ntx = (g.X + TL::TX - 1) / TL::TX;
   const uint32_t nty = (g.Y + TL::TY - 1) / TL::TY;
@@ -1509,9 +1527,9 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
                             ? ((lx == 0 ? 1u : 0u) | (lx == ex - 1 ? 2u : 0u) | (ly == 0 ? 4u : 0u) |
                                (ly == ey - 1 ? 8u : 0u) | (lz == 0 ? 16u : 0u) | (lz == ez - 1 ? 32u : 0u))
                             : 63u;
-    const uint32_t ca = code & 15u, cd = code >> 4;
-    const uint32_t pa = (sface[ca] & on) ? i : i + sloc[ca];  // SELF: sloc 0
-    const uint32_t pd = (sface[cd] & on) ? i : i + sloc[cd];
+    const uint2 e = scode[code];  // SELF: offset 0, no face
+    const uint32_t pa = (e.y & on) ? i : i + static_cast<int32_t>(static_cast<int16_t>(e.x & 0xFFFFu));
+    const uint32_t pd = ((e.y >> 8) & on) ? i : i + (static_cast<int32_t>(e.x) >> 16);
     own[j] = pa | (pd << 16);
     ptr[i] = own[j];
   }
