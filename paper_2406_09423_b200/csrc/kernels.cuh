@@ -1679,30 +1679,33 @@ __global__ void __launch_bounds__(256) k_exit_jump_tiles(TileStore ts, uint32_t*
     const uint32_t n = ts.Ecnt[b * 2 + fam];
     const size_t o = (static_cast<size_t>(b) * 2 + fam) * ts.surface;
     uint32_t* fin = fam ? finm : finM;
-    // block-uniform trip count (block_reserve); two exits per thread per step
-    // so the two 3-deep gather chains overlap
-    for (uint32_t kb = 0; kb < n; kb += 2 * blockDim.x) {
-      uint32_t e[2], l[2], ll[2];
-      bool live[2], keep[2] = {false, false};
+    // block-uniform trip count (block_reserve); four exits per thread per step
+    // so the 3-deep gather chains overlap
+    for (uint32_t kb = 0; kb < n; kb += 4 * blockDim.x) {
+      uint32_t e[4], l[4], ll[4];
+      bool live[4], keep[4] = {false, false, false, false};
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
+      for (int q = 0; q < 4; ++q) {
         const uint32_t k = kb + threadIdx.x + q * blockDim.x;
         live[q] = k < n;
         e[q] = live[q] ? ts.E[o + k] : 0u;
       }
 #pragma unroll
-      for (int q = 0; q < 2; ++q) l[q] = live[q] ? fin[e[q]] : 0u;
+      for (int q = 0; q < 4; ++q) l[q] = live[q] ? fin[e[q]] : 0u;
 #pragma unroll
-      for (int q = 0; q < 2; ++q) ll[q] = live[q] ? fin[l[q]] : 0u;
+      for (int q = 0; q < 4; ++q) ll[q] = live[q] ? fin[l[q]] : 0u;
 #pragma unroll
-      for (int q = 0; q < 2; ++q)
+      for (int q = 0; q < 4; ++q)
         if (live[q] && ll[q] != l[q]) {
           fin[e[q]] = ll[q];
           keep[q] = fin[ll[q]] != ll[q];
         }
-      uint32_t pos = block_reserve((keep[0] ? 1u : 0u) + (keep[1] ? 1u : 0u), cnt_out + fam);
+      uint32_t nk = 0;
 #pragma unroll
-      for (int q = 0; q < 2; ++q)
+      for (int q = 0; q < 4; ++q) nk += keep[q] ? 1u : 0u;
+      uint32_t pos = block_reserve(nk, cnt_out + fam);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
         if (keep[q]) (fam ? out_d : out_a)[pos++] = e[q];
     }
   }
