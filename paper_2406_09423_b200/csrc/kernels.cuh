@@ -1650,18 +1650,18 @@ __global__ void __launch_bounds__(256) k_exit_reset(TileStore ts, const uint32_t
     const size_t o = (static_cast<size_t>(b) * 2 + fam) * ts.surface;
     uint32_t* fin = fam ? finm : finM;
     const uint32_t* prov = fam ? m : M;
-    // four exits per thread per step: their loads and gathers overlap
-    for (uint32_t k0 = threadIdx.x; k0 < n; k0 += 4 * blockDim.x) {
-      uint32_t e[4], p[4];
+    // eight exits per thread per step: their loads and gathers overlap
+    for (uint32_t k0 = threadIdx.x; k0 < n; k0 += 8 * blockDim.x) {
+      uint32_t e[8], p[8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < 8; ++q) {
         const uint32_t k = k0 + q * blockDim.x;
         e[q] = k < n ? ts.E[o + k] : kNoTarget;
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q) p[q] = e[q] != kNoTarget ? __ldg(prov + e[q]) : 0u;
+      for (int q = 0; q < 8; ++q) p[q] = e[q] != kNoTarget ? __ldg(prov + e[q]) : 0u;
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < 8; ++q)
         if (e[q] != kNoTarget) fin[e[q]] = p[q];
     }
   }
