@@ -51,9 +51,21 @@ UNIT = "Mvertices/s"
 # step's own counters where a launch covers less than the whole field.  Classes
 # without an entry (persistent subloop, gathers over lists) are latency-bound
 # and not roofline-graded.
-def alg_bytes(cls: str, es: int, n: int, st, launches: int) -> float:
+# Freudenthal rings (grid.cpp:8-16): |{t} ∪ N(t)| and |2-ring of t| (2D, 3D)
+RING1 = {2: 7, 3: 15}
+RING2 = {2: 19, 3: 65}
+
+
+def alg_bytes(cls: str, es: int, n: int, st, launches: int, ndims: int = 3) -> float:
     tile = 8192
+    r1, r2 = RING1[ndims], RING2[ndims]
     return {
+        # persistent C loop (run_subloop, edit_engine.cpp:246-278), per worklist
+        # item: list entry 4 + its code 1 + claim stamp 4 + next-list entry 4;
+        # per applied edit: the lowered value written, the values of the 2-ring
+        # of t (the inputs of every code the edit can change, mss.cpp:17-29) and
+        # the 1-ring's codes (g code written, f code read for the kind test)
+        "subloop": 13 * st.subloop_items + (es + r2 * es + 2 * r1) * st.subloop_edits,
         "validate": 2 * es * n * launches,               # read f and fhat
         "directions": (es + 1) * n * launches,           # read values, write one code byte
         "detect_kind": 2 * n * launches,                 # full sweeps: fdir + gdir
@@ -191,8 +203,9 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def cpu_reference_run(cfg, dims, dtype, threads, steps=1):
-    """The unmodified reference derive_edits on the host (oracle/_ref): returns (times, stats)."""
+def cpu_reference_run(cfg, dims, dtype, threads, steps=1, want_inputs=False):
+    """The unmodified reference derive_edits on the host (oracle/_ref): returns
+    (times, stats) or, with want_inputs, (times, stats, (f, fhat, xi), result)."""
     import oracle as O
     if not O.have_ref():
         raise RuntimeError("oracle/_ref/libmssz_ref.so missing (build() it in the build container)")
@@ -211,7 +224,47 @@ def cpu_reference_run(cfg, dims, dtype, threads, steps=1):
         t = time.perf_counter()
         res = R.derive_edits(list(dims), f, fh, xi, subloop_cap=cfg.subloop_cap, threads=threads)
         times.append(time.perf_counter() - t)
+    if want_inputs:
+        return times, res.stats, (f, fh, xi), res
     return times, res.stats
+
+
+STAT_KEYS = ("outer_iterations", "c_passes", "sub_iterations", "r_iterations",
+             "effective_edits", "touched")
+
+
+def same_input_comparison(P, cfg, sdims, inputs, ref_res, ref_s, device=0):
+    """The B200 engine on exactly the reference arm's input (its own generator
+    and base codec), through the public host API: EditStats side by side
+    (edit_engine.hpp:54-68) and the same-input speed ratio."""
+    f, fh, xi = inputs
+    topo = P.build_topology(list(sdims))
+    opts = P.DeriveOptions(subloop_cap=cfg.subloop_cap, device=device)
+    P.derive_edits(topo, f, fh, xi, opts)  # warm (workspace sized)
+    walls, st, e = [], None, None
+    for _ in range(3):
+        st = P.EditStats()
+        t = time.perf_counter()
+        e = P.derive_edits(topo, f, fh, xi, opts, st)
+        walls.append(time.perf_counter() - t)
+    gpu_s = min(walls)
+    rt = ref_res.stats["touched"]
+    gpu = {k: getattr(st, k) for k in STAT_KEYS}
+    ref = {k: ref_res.stats[k] for k in STAT_KEYS}
+    common = int(np.intersect1d(e.indices, ref_res.indices, assume_unique=True).size)
+    return {
+        "input": "identical arrays: the reference's generate_synthetic + compress_base outputs",
+        "dims": list(sdims), "vertices": int(np.prod(sdims)),
+        "gpu_edit_stats": gpu, "reference_edit_stats": ref,
+        "touched_diff": int(st.touched) - int(rt), "touched_tolerance": max(4, int(1e-4 * rt)),
+        "edit_sets_identical": bool(np.array_equal(e.indices, ref_res.indices)
+                                   and e.values.tobytes() == ref_res.values.tobytes()),
+        "edit_index_overlap": {"gpu": int(e.indices.size), "reference": int(ref_res.indices.size),
+                               "common": common},
+        "gpu_e2e_s": gpu_s, "reference_s": ref_s,
+        "same_input_speedup_e2e": ref_s / gpu_s,
+        "gpu_api": "derive_edits (mssz_cu_derive_edits, host buffers in and out)",
+    }
 
 
 def run_reference_arm(args, cfg, dist):
@@ -227,13 +280,18 @@ def run_reference_arm(args, cfg, dist):
     mean = statistics.mean(timed)
     value = n / mean / 1e6
     sample = f"{cfg.name} kind={cfg.kind} at {'x'.join(map(str, dims))} ({n} vertices), rel {cfg.rel}"
+    same = list(dims) == list(cfg.dims)
+    workload = cfg.note if same else (
+        f"bounded CPU sample of {cfg.name} ({cfg.note}): the same generator at "
+        f"{'x'.join(map(str, dims))}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": mean * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-        "config": {"workload": cfg.note, "sample_dims": list(dims), "rel_eb": cfg.rel,
-                   "subloop_cap": cfg.subloop_cap, "parallelism": "openmp"},
+        "config": {"workload": workload, "config_id": cfg.name, "config_dims": list(cfg.dims),
+                   "sample_dims": list(dims), "same_config": same, "rel_eb": cfg.rel,
+                   "subloop_cap": cfg.subloop_cap, "parallelism": f"openmp x{threads}"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -335,7 +393,7 @@ def main():
     if prof_stats is not None:
         kp = prof_stats.kernel_profile()
         cand = {k: v["ms"] for k, v in kp.items()
-                if v["launches"] and alg_bytes(k, es, n_local, prof_stats, v["launches"])}
+                if v["launches"] and alg_bytes(k, es, n_local, prof_stats, v["launches"], len(dims))}
         top = max(cand, key=cand.get) if cand else None
     timed_profile = P.profile_mask(top) if top else False
 
@@ -372,14 +430,14 @@ def main():
         total_ms = sum(v["ms"] for v in prof.values())
         graded = {}
         for k, v in prof.items():
-            tot = alg_bytes(k, es, n_local, prof_stats, v["launches"])
+            tot = alg_bytes(k, es, n_local, prof_stats, v["launches"], len(dims))
             if tot:
                 graded[k] = {"launches": v["launches"], "ms": v["ms"], "bytes": tot,
                              "achieved_GBps": tot / (v["ms"] * 1e-3) / 1e9}
         # the graded kernel: achieved from its launches inside the timed steps
         t_launch = sum(s.kernel_profile()[top]["launches"] for s in stats)
         t_ms = sum(s.kernel_profile()[top]["ms"] for s in stats)
-        t_bytes = sum(alg_bytes(top, es, n_local, s, s.kernel_profile()[top]["launches"]) for s in stats)
+        t_bytes = sum(alg_bytes(top, es, n_local, s, s.kernel_profile()[top]["launches"], len(dims)) for s in stats)
         per_launch_ms = t_ms / t_launch
         bytes_per_launch = t_bytes / t_launch
         achieved = t_bytes / (t_ms * 1e-3) / 1e9
@@ -403,6 +461,7 @@ def main():
                                  "frac_of_peak": gbs / peak, "source": "profiles/ncu_traffic_c4.json"})
         roofline = {"kernel": top, "bound": "hbm", "achieved": achieved, "peak": peak,
                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                    "dram_over_algorithmic": (traffic / bytes_per_launch) if traffic else None,
                     "peak_source": peak_src,
                     "alg_bytes_per_launch": bytes_per_launch,
                     "mean_launch_us": per_launch_ms * 1e3,
@@ -512,13 +571,18 @@ def main():
         threads = os.cpu_count() or 1
         os.environ.setdefault("OMP_WAIT_POLICY", "active")
         try:
-            times, cst = cpu_reference_run(cfg, sdims, dtype, threads, steps=1)
+            times, cst, inputs, ref_res = cpu_reference_run(cfg, sdims, dtype, threads, steps=1,
+                                                            want_inputs=True)
             sn = int(np.prod(sdims))
             cpu = {"value": sn / times[0] / 1e6, "unit": UNIT, "cores": threads,
                    "kind": "reference",
                    "sample": f"derive_edits on {cfg.kind} {'x'.join(map(str, sdims))} "
                              f"({sn} vertices), rel {cfg.rel}, {times[0]:.2f} s",
-                   "edit_stats": cst}
+                   "same_config": list(sdims) == list(dims),
+                   "edit_stats": cst,
+                   "same_input": same_input_comparison(P, cfg, sdims, inputs, ref_res, times[0],
+                                                       dist.local)}
+            del inputs, ref_res
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": UNIT, "cores": threads, "kind": "reference",
                    "sample": f"unavailable: {e}"}

@@ -15,6 +15,7 @@
 
 #include <array>
 #include <cstdint>
+#include <exception>
 #include <functional>
 #include <span>
 #include <stdexcept>
@@ -136,10 +137,25 @@ struct Api<double> {
   static constexpr auto decompress_base = mssz_cu_decompress_base_f64;
   static constexpr auto encode_edits = mssz_cu_encode_edits_f64;
 };
+// on_batch across the C ABI: an exception thrown by the callback is caught
+// here (it must not unwind through extern "C"), the engine is told to abort
+// (nonzero), and derive_edits rethrows it -- the reference's exception
+// propagation out of derive_edits (edit_engine.cpp:275, :364).
 template <class T>
-void batch_trampoline(const void* g, std::uint64_t n, void* user) {
-  auto* fn = static_cast<std::function<void(std::span<const T>)>*>(user);
-  (*fn)(std::span<const T>(static_cast<const T*>(g), n));
+struct BatchCall {
+  std::function<void(std::span<const T>)> fn;
+  std::exception_ptr error;
+};
+template <class T>
+int batch_trampoline(const void* g, std::uint64_t n, void* user) {
+  auto* call = static_cast<BatchCall<T>*>(user);
+  try {
+    call->fn(std::span<const T>(static_cast<const T*>(g), n));
+    return 0;
+  } catch (...) {
+    call->error = std::current_exception();
+    return 1;
+  }
 }
 }  // namespace detail
 
@@ -155,17 +171,19 @@ EditSet<T> derive_edits(const GridTopology& topo, const T* original, const T* de
   o.r_cap = opts.r_cap;
   o.force = opts.force ? 1 : 0;
   o.device = opts.device;
-  auto cb = opts.on_batch;
-  if (cb) {
+  detail::BatchCall<T> call{opts.on_batch, nullptr};
+  if (call.fn) {
     o.on_batch = &detail::batch_trampoline<T>;
-    o.on_batch_user = &cb;
+    o.on_batch_user = &call;
   }
   std::uint64_t* idx = nullptr;
   T* val = nullptr;
   std::uint64_t count = 0;
   EditStats st;
-  check(detail::Api<T>::derive(topo.ndims, topo.dims.data(), original, decompressed, xi, &o,
-                               &idx, &val, &count, &st));
+  const int rc = detail::Api<T>::derive(topo.ndims, topo.dims.data(), original, decompressed, xi,
+                                        &o, &idx, &val, &count, &st);
+  if (rc == MSSZ_CU_ERR_CALLBACK && call.error) std::rethrow_exception(call.error);
+  check(rc);
   EditSet<T> set;
   set.indices.assign(idx, idx + count);
   set.values.assign(val, val + count);

@@ -29,7 +29,20 @@
  *       element-wise EditState<T>::lower_step (edit_engine.cpp:75-86) and
  *       representable_floor (edit_engine.cpp:22-29).
  *   mssz_cu_apply_edits_{f32,f64}
- *       replaces  apply_edits<T> (edit_engine.hpp:188-190, edit_engine.cpp:437-450).
+ *       replaces  apply_edits<T> (edit_engine.hpp:188-190, edit_engine.cpp:437-450);
+ *                 indices are applied in order (a repeated index: the last value
+ *                 wins); an out-of-range index fails with corrupt_archive and
+ *                 writes no output.
+ *   mssz_cu_r_targets_{f32,f64}
+ *       one R-loop batch's target set (run_r_loop, edit_engine.cpp:336-352:
+ *                 collect_mismatched + find_troublemaker :293-315 + claim) for an
+ *                 (original, edited) pair, computed by the engine's tiled pass
+ *                 (mode 0) or its sparse Up(X) pass (mode 1).  targets: caller
+ *                 buffer of n entries, sorted, distinct.  info = {false critical
+ *                 points of the pair (the R gate, :338), divergent mismatched
+ *                 (vertex, family) pairs = distinct troublemaker sources v_i,
+ *                 path used (0 tiled, 1 sparse; mode 1 falls back to 0 when
+ *                 Up(X) is too large)}.  Parity harness entry point.
  *
  * Conventions (mirroring errors.hpp:9-16): every function returns 0 or the
  * reference ErrKind value (2 usage, 3 io, 4 bound_violation, 5 non_convergence,
@@ -58,23 +71,43 @@ extern "C" {
 #define MSSZ_CU_ERR_NON_CONVERGENCE 5
 #define MSSZ_CU_ERR_CORRUPT_ARCHIVE 6
 #define MSSZ_CU_ERR_INTERNAL 7
+#define MSSZ_CU_ERR_CALLBACK 98 /* on_batch returned nonzero: the correction was abandoned */
 #define MSSZ_CU_ERR_CUDA 99
 
 /* Mirrors DeriveOptions<T> (edit_engine.hpp:70-82).  ExecPolicy becomes a
  * device choice; on_batch becomes an optional host callback (debug/parity
- * mode: the device loop then stops after every batch so the host can read g). */
+ * mode: the device loop then stops after every batch so the host can read g).
+ * In the reference an exception thrown by on_batch aborts derive_edits; here the
+ * callback returns nonzero to abort, and the call returns MSSZ_CU_ERR_CALLBACK
+ * (the language bindings re-raise the callback's own exception).
+ * on_batch_mode: MSSZ_CU_ON_BATCH_EVERY (0) = after every fix batch, exactly the
+ * reference's call sites (edit_engine.cpp:275, :364); MSSZ_CU_ON_BATCH_PHASES (1)
+ * = only after each complete C pass (all four subloops, :280-291) and after
+ * each R iteration, with the device loop running at full speed in between
+ * (snapshots of large fields for parity checks). */
 typedef struct mssz_cu_options {
   uint64_t outer_cap;   /* default 1000 */
   uint64_t subloop_cap; /* default 640, per run_subloop invocation */
   uint64_t r_cap;       /* default 100000, per run_r_loop invocation */
   int32_t force;        /* accept |f - fhat| > xi inputs */
   int32_t device;       /* CUDA ordinal; -1 = current device */
-  void (*on_batch)(const void* g_host, uint64_t n, void* user); /* NULL = off */
+  int (*on_batch)(const void* g_host, uint64_t n, void* user); /* NULL = off; nonzero = abort */
   void* on_batch_user;
   int32_t profile; /* CUDA-event kernel timing into stats.kernel_ms: bit 0 = every class,
                       bit (c + 1) = class c only (MSSZ_CU_PROF_*) */
-  int32_t reserved;
+  int32_t on_batch_mode; /* MSSZ_CU_ON_BATCH_EVERY / MSSZ_CU_ON_BATCH_PHASES */
 } mssz_cu_options;
+
+#define MSSZ_CU_ON_BATCH_EVERY 0
+#define MSSZ_CU_ON_BATCH_PHASES 1
+
+/* Inside an on_batch callback: what the snapshot is.  out = {kind, outer
+ * iteration (1-based), index (1-based C pass, or R iteration, within that outer
+ * iteration; for kind BATCH the C pass in progress)}. */
+#define MSSZ_CU_PHASE_BATCH 0       /* a C fix batch (mode EVERY) */
+#define MSSZ_CU_PHASE_C_PASS 1      /* a complete C pass (mode PHASES) */
+#define MSSZ_CU_PHASE_R_ITERATION 2 /* an R iteration (both modes) */
+int mssz_cu_batch_phase(uint64_t out[3]);
 
 /* kernel classes of mssz_cu_stats.kernel_ms / kernel_count */
 #define MSSZ_CU_PROF_VALIDATE 0
@@ -121,6 +154,9 @@ typedef struct mssz_cu_stats {
   uint64_t sparse_iterations; /* R iterations resolved by the sparse Up(X) pass */
   uint64_t sparse_up;         /* sum of |Up(X)| over sparse passes */
   uint64_t rfix_divergent;    /* (vertex, family) pairs k_rfix_tiles resolved a label for */
+  uint64_t subloop_items;     /* worklist items fixed by the persistent C-loop kernel */
+  uint64_t subloop_edits;     /* edits applied by the persistent C-loop kernel (its batches) */
+  uint64_t skipped_subloops;  /* subloops skipped without a launch (list provably empty) */
   uint64_t kernel_count[MSSZ_CU_PROF_CLASSES]; /* launches per kernel class */
   double kernel_ms[MSSZ_CU_PROF_CLASSES];      /* device ms per profiled class */
 } mssz_cu_stats;
@@ -163,7 +199,10 @@ int mssz_cu_release_workspace(int device);
                                uint8_t* moved);                                                \
   int mssz_cu_representable_floor_##SUF(uint64_t n, const T* f, double xi, T* out);           \
   int mssz_cu_apply_edits_##SUF(uint64_t n, const T* decompressed, const uint64_t* indices,   \
-                                const T* values, uint64_t count, T* out);
+                                const T* values, uint64_t count, T* out);                     \
+  int mssz_cu_r_targets_##SUF(int ndims, const uint64_t* dims, const T* original,              \
+                              const T* edited, int mode, uint64_t* targets, uint64_t* count,   \
+                              uint64_t info[3]);
 
 MSSZ_CU_DECLARE_TYPED(f32, float)
 MSSZ_CU_DECLARE_TYPED(f64, double)

@@ -140,18 +140,18 @@ class _Lib:
             msg = self._fn("last_error")().decode()
             raise CheckerError(rc, msg)
 
-    def compute_directions(self, dims, values: np.ndarray):
+    def compute_directions(self, dims, values: np.ndarray, threads: int = 1):
         values = np.ascontiguousarray(values)
         n = int(np.prod(dims))
         asc = np.empty(n, np.uint64)
         desc = np.empty(n, np.uint64)
         args = [len(dims), _dims_arr(dims), _ptr(values), _ptr(asc), _ptr(desc)]
         if self.prefix == "mssz_ref_":
-            args.append(1)
+            args.append(threads)
         self._check(self._fn("compute_directions_" + _suffix(values.dtype))(*args))
         return asc, desc
 
-    def compute_labels(self, dims, asc: np.ndarray, desc: np.ndarray):
+    def compute_labels(self, dims, asc: np.ndarray, desc: np.ndarray, threads: int = 1):
         n = int(np.prod(dims))
         M = np.empty(n, np.uint64)
         m = np.empty(n, np.uint64)
@@ -159,20 +159,25 @@ class _Lib:
         desc = np.ascontiguousarray(desc, np.uint64)
         args = [len(dims), _dims_arr(dims), _ptr(asc), _ptr(desc), _ptr(M), _ptr(m)]
         if self.prefix == "mssz_ref_":
-            args.append(1)
+            args.append(threads)
         self._check(self._fn("compute_labels")(*args))
         return M, m
 
-    def detect_false_critical(self, dims, f: np.ndarray, g: np.ndarray, xi: float = 1.0):
+    def detect_false_critical(self, dims, f: np.ndarray, g: np.ndarray, xi: float = 1.0,
+                              threads: int = 1):
         n = int(np.prod(dims))
         counts = np.zeros(4, np.uint64)
         lists = np.zeros(4 * n, np.uint64)
         suf = _suffix(f.dtype)
         args = [len(dims), _dims_arr(dims), _ptr(f), _ptr(g)]
+        name = "detect_false_critical_"
         if self.prefix == "mssz_ref_":
             args.append(C.c_double(xi))
         args += [_ptr(counts), _ptr(lists)]
-        self._check(self._fn("detect_false_critical_" + suf)(*args))
+        if self.prefix == "mssz_ref_" and threads != 1:
+            name = "detect_false_critical_mt_"
+            args.append(threads)
+        self._check(self._fn(name + suf)(*args))
         return [lists[k * n : k * n + int(counts[k])].copy() for k in range(4)]
 
     def _derive(self, fn, dims, f, fhat, xi, opts, record_batches):
@@ -258,6 +263,21 @@ class Ref(_Lib):
             len(dims), _dims_arr(dims), _ptr(f), _ptr(g), C.c_double(xi), C.c_uint64(v),
             max_steps, _ptr(trace), C.byref(steps), _ptr(floor)))
         return trace[: steps.value + 1], floor[0]
+
+    def r_targets(self, dims, f, g, threads=0):
+        """run_r_loop's target collection (edit_engine.cpp:336-352) on (f, g):
+        (sorted distinct targets, false critical points, distinct (v_i, family)
+        sources, mismatched vertices)."""
+        f = np.ascontiguousarray(f)
+        g = np.ascontiguousarray(g, f.dtype)
+        n = int(np.prod(dims))
+        out = np.empty(2 * n, np.uint64)
+        cnt = C.c_uint64()
+        info = np.zeros(3, np.uint64)
+        self._check(self._fn("r_targets_" + _suffix(f.dtype))(
+            len(dims), _dims_arr(dims), _ptr(f), _ptr(g), threads, _ptr(out), C.byref(cnt),
+            _ptr(info)))
+        return out[: cnt.value].copy(), int(info[0]), int(info[1]), int(info[2])
 
     def encode_edits(self, indices: np.ndarray, values: np.ndarray, codec: int = 1) -> bytes:
         """encode_edits<T> (edit_codec.cpp:188-222): the reference edit payload."""

@@ -118,6 +118,8 @@ static int jump_to_fixpoint(uint64_t n, const uint64_t* parent, uint64_t* cur, u
   uint64_t* dst = next;
   for (int round = 0; round < cap; ++round) {
     int changed = 0;
+    /* round-synchronous (reads src, writes dst): thread-count invariant */
+#pragma omp parallel for schedule(static) reduction(| : changed)
     for (uint64_t i = 0; i < n; ++i) {
       const uint64_t hop = src[src[i]];
       dst[i] = hop;

@@ -10,6 +10,7 @@
 //   oracle_labels<T>       mss.hpp:66-67 / mss.cpp:99-120
 //   EditState::detect_false_critical / lower_step / find_troublemaker
 //                          edit_engine.hpp:95-120
+//   run_r_loop's target collection (r_targets) edit_engine.cpp:336-352
 //   generate_synthetic<T>  field.hpp:343-345 / field.cpp:229-250
 //   compress_base<T>       base_codec.hpp:198-199 / base_codec.cpp:76-120
 //   resolve_bound<T>       field.hpp:320-321 / field.cpp:42-50
@@ -17,6 +18,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -160,10 +162,10 @@ int oracle_labels_impl(int ndims, const uint64_t* dims, const T* values, uint64_
 // counts[4] per first-match class; lists is 4*N u64 (class k at lists + k*N)
 template <class T>
 int detect_impl(int ndims, const uint64_t* dims, const T* f, const T* g, double xi,
-                uint64_t* counts, uint64_t* lists) {
+                uint64_t* counts, uint64_t* lists, int threads = 1) {
   return guarded([&] {
     GridTopology topo = topo_of(ndims, dims);
-    EditState<T> state(topo, f, g, xi, ExecPolicy::serial_policy());
+    EditState<T> state(topo, f, g, xi, make_policy(threads));
     const FalseCriticalReport& r = state.detect_false_critical();
     const std::vector<VertexId>* ls[4] = {&r.fp_max, &r.fp_min, &r.fn_max, &r.fn_min};
     for (int k = 0; k < 4; ++k) {
@@ -204,6 +206,67 @@ int troublemaker_impl(int ndims, const uint64_t* dims, const T* f, const T* g, d
                                                    : EditState<T>::LineKind::ascending);
     *vi = r.first;
     *vt = r.second;
+  });
+}
+
+}  // namespace
+
+// The reference grants its test suite access to EditState's private R-loop
+// steps through this friend (edit_engine.hpp:173); the shim uses it to run
+// one R batch's target collection exactly as run_r_loop does.
+namespace mssz {
+struct EditEngineTestAccess {
+  template <class T>
+  static void compute_g_labels(EditState<T>& s) { s.compute_g_labels(); }
+  template <class T>
+  static std::uint64_t collect_mismatched(const EditState<T>& s, std::vector<VertexId>& out) {
+    return s.collect_mismatched(out);
+  }
+  template <class T>
+  static const SegmentationLabels& g_labels(const EditState<T>& s) { return s.g_labels_; }
+};
+}  // namespace mssz
+
+namespace {
+
+// One R batch's target set, run_r_loop (edit_engine.cpp:336-352): labels of g,
+// collect_mismatched, find_troublemaker per mismatched vertex and family; the
+// claim dedupe becomes sort + unique.  info = {false critical points of (f, g)
+// (the gate, :338), distinct (v_i, family) troublemaker sources, mismatched
+// vertices}.  The gate is reported, not applied, so a caller can also ask for
+// targets of a state the loop would hand back to the C-loop.
+template <class T>
+int r_targets_impl(int ndims, const uint64_t* dims, const T* f, const T* g, int threads,
+                   uint64_t* targets, uint64_t* count, uint64_t* info) {
+  return guarded([&] {
+    GridTopology topo = topo_of(ndims, dims);
+    EditState<T> state(topo, f, g, 1.0, make_policy(threads));
+    state.refresh_directions();
+    info[0] = state.detect_false_critical().total();
+    EditEngineTestAccess::compute_g_labels(state);
+    std::vector<VertexId> mismatched;
+    info[2] = EditEngineTestAccess::collect_mismatched(state, mismatched);
+    const SegmentationLabels& gl = EditEngineTestAccess::g_labels(state);
+    const SegmentationLabels& fl = state.original_labels();
+    std::vector<VertexId> t, src;
+    for (VertexId v : mismatched) {
+      if (gl.max_label[v] != fl.max_label[v]) {
+        auto [vi, vt] = state.find_troublemaker(v, EditState<T>::LineKind::ascending);
+        t.push_back(vt);
+        src.push_back(vi * 2);
+      }
+      if (gl.min_label[v] != fl.min_label[v]) {
+        auto [vi, vt] = state.find_troublemaker(v, EditState<T>::LineKind::descending);
+        t.push_back(vt);
+        src.push_back(vi * 2 + 1);
+      }
+    }
+    std::sort(t.begin(), t.end());
+    t.erase(std::unique(t.begin(), t.end()), t.end());
+    std::sort(src.begin(), src.end());
+    info[1] = static_cast<uint64_t>(std::unique(src.begin(), src.end()) - src.begin());
+    std::copy(t.begin(), t.end(), targets);
+    *count = t.size();
   });
 }
 
@@ -263,6 +326,11 @@ extern "C" {
                                            uint64_t* lists) {                                \
     return detect_impl<T>(ndims, dims, f, g, xi, counts, lists);                             \
   }                                                                                          \
+  int mssz_ref_detect_false_critical_mt_##SUF(int ndims, const uint64_t* dims, const T* f,   \
+                                              const T* g, double xi, uint64_t* counts,       \
+                                              uint64_t* lists, int threads) {                \
+    return detect_impl<T>(ndims, dims, f, g, xi, counts, lists, threads);                    \
+  }                                                                                          \
   int mssz_ref_lower_step_##SUF(int ndims, const uint64_t* dims, const T* f, const T* g,     \
                                 double xi, uint64_t v, int max_steps, T* trace, int* steps,  \
                                 T* floor_out) {                                              \
@@ -272,6 +340,11 @@ extern "C" {
                                        const T* g, double xi, uint64_t v, int descending,    \
                                        uint64_t* vi, uint64_t* vt) {                         \
     return troublemaker_impl<T>(ndims, dims, f, g, xi, v, descending, vi, vt);               \
+  }                                                                                          \
+  int mssz_ref_r_targets_##SUF(int ndims, const uint64_t* dims, const T* f, const T* g,      \
+                               int threads, uint64_t* targets, uint64_t* count,              \
+                               uint64_t* info) {                                             \
+    return r_targets_impl<T>(ndims, dims, f, g, threads, targets, count, info);              \
   }                                                                                          \
   int mssz_ref_generate_##SUF(int kind, int ndims, const uint64_t* dims, uint64_t seed,      \
                               T* out) {                                                      \

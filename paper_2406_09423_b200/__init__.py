@@ -49,7 +49,11 @@ class ErrKind(IntEnum):
     non_convergence = 5
     corrupt_archive = 6
     internal = 7
+    callback = 98  # on_batch raised: the correction was abandoned (the exception is re-raised)
     cuda = 99
+
+
+ERR_CALLBACK = 98
 
 
 class Error(RuntimeError):
@@ -123,6 +127,10 @@ class DeriveOptions:
     force: bool = False
     device: int = -1
     on_batch: Optional[Callable[[np.ndarray], None]] = None
+    # "every": after every fix batch (the reference's call sites); "phases": only
+    # after each complete C pass and each R iteration, the device loop running
+    # at full speed in between (snapshots of large fields)
+    on_batch_mode: str = "every"
     # per-kernel CUDA-event timing into EditStats.kernel_ms: True = every class,
     # or an int mask from profile_mask(...) for selected classes only
     profile: Union[bool, int] = False
@@ -156,6 +164,9 @@ class EditStats:
     sparse_iterations: int = 0
     sparse_up: int = 0
     rfix_divergent: int = 0
+    subloop_items: int = 0
+    subloop_edits: int = 0
+    skipped_subloops: int = 0
     kernel_count: list = field(default_factory=lambda: [0] * 16)
     kernel_ms: list = field(default_factory=lambda: [0.0] * 16)
 
@@ -237,7 +248,7 @@ class _Options(C.Structure):
         ("outer_cap", C.c_uint64), ("subloop_cap", C.c_uint64), ("r_cap", C.c_uint64),
         ("force", C.c_int32), ("device", C.c_int32),
         ("on_batch", C.c_void_p), ("on_batch_user", C.c_void_p),
-        ("profile", C.c_int32), ("reserved", C.c_int32),
+        ("profile", C.c_int32), ("on_batch_mode", C.c_int32),
     ]
 
 
@@ -254,6 +265,8 @@ class _Stats(C.Structure):
         ("kernel_launches", C.c_uint64), ("big_batches", C.c_uint64),
         ("huge_batches", C.c_uint64), ("label_tiles", C.c_uint64), ("rfix_tiles", C.c_uint64),
         ("sparse_iterations", C.c_uint64), ("sparse_up", C.c_uint64), ("rfix_divergent", C.c_uint64),
+        ("subloop_items", C.c_uint64), ("subloop_edits", C.c_uint64),
+        ("skipped_subloops", C.c_uint64),
         ("kernel_count", C.c_uint64 * 16), ("kernel_ms", C.c_double * 16),
     ]
 
@@ -275,21 +288,21 @@ def profile_mask(*classes: str) -> int:
     return sum(1 << (PROF_CLASSES.index(c) + 1) for c in classes)
 
 
-_BATCH_CB = C.CFUNCTYPE(None, C.c_void_p, C.c_uint64, C.c_void_p)
+_BATCH_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.c_void_p)
 
 # every symbol include/mssz_cuda.h declares (tests check the exports)
 EXPORTS = [
     "mssz_cu_default_options", "mssz_cu_last_error", "mssz_cu_free", "mssz_cu_device_count",
     "mssz_cu_version", "mssz_cu_release_workspace", "mssz_cu_compute_labels",
     "mssz_cu_classify_critical", "mssz_cu_slab_range", "mssz_cu_comm_unique_id",
-    "mssz_cu_comm_init", "mssz_cu_comm_destroy",
+    "mssz_cu_comm_init", "mssz_cu_comm_destroy", "mssz_cu_batch_phase",
 ] + [
     f"mssz_cu_{name}_{suf}" for suf in ("f32", "f64") for name in (
         "derive_edits", "derive_edits_into", "derive_edits_device", "compute_directions",
         "compute_direction_codes", "detect_false_critical", "detect_kind", "lower_step",
         "representable_floor", "apply_edits", "derive_edits_slab", "derive_edits_slab_device",
         "derive_edits_slabs_local", "verify", "verify_device", "segmentation", "compress_base",
-        "decompress_base", "encode_edits")
+        "decompress_base", "encode_edits", "r_targets")
 ]
 
 _lib = None
@@ -359,19 +372,53 @@ def _field(topo: GridTopology, a, name: str, dtype=None) -> np.ndarray:
 
 def _options(opts: Optional[DeriveOptions], dtype, keep: list) -> _Options:
     o = opts or DeriveOptions()
+    if o.on_batch_mode not in ("every", "phases"):
+        raise Error(ErrKind.usage, f"on_batch_mode must be 'every' or 'phases', not {o.on_batch_mode!r}")
     co = _Options(o.outer_cap, o.subloop_cap, o.r_cap, int(o.force), o.device, None, None,
-                  int(o.profile), 0)
+                  int(o.profile), 0 if o.on_batch_mode == "every" else 1)
     if o.on_batch is not None:
         ctype = _ctype(dtype)
 
         def _cb(ptr, n, user):
-            arr = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(ctype)), shape=(n,))
-            o.on_batch(arr.copy())
+            # an exception must not be swallowed by ctypes: store it, tell the
+            # engine to abort (nonzero), re-raise it after the call (_check_cb)
+            try:
+                arr = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(ctype)), shape=(n,))
+                o.on_batch(arr.copy())
+                return 0
+            except BaseException as e:  # noqa: BLE001 - re-raised by _check_cb
+                keep.append(_CallbackFailure(e))
+                return 1
 
         cb = _BATCH_CB(_cb)
         keep.append(cb)
         co.on_batch = C.cast(cb, C.c_void_p)
     return co
+
+
+class _CallbackFailure:
+    def __init__(self, exc: BaseException):
+        self.exc = exc
+
+
+PHASE_KINDS = ("batch", "c_pass", "r_iteration")
+
+
+def batch_phase() -> tuple:
+    """Inside an on_batch callback: (kind, outer iteration, index) of the snapshot,
+    kind in PHASE_KINDS (mssz_cu_batch_phase)."""
+    out = np.zeros(3, np.uint64)
+    _check(library().mssz_cu_batch_phase(_p(out)))
+    return PHASE_KINDS[int(out[0])], int(out[1]), int(out[2])
+
+
+def _check_cb(rc: int, keep: list) -> None:
+    """_check, re-raising an on_batch exception as the reference's would propagate."""
+    if rc == ERR_CALLBACK:
+        for k in keep:
+            if isinstance(k, _CallbackFailure):
+                raise k.exc
+    _check(rc)
 
 
 def derive_edits(topo: GridTopology, original, decompressed, xi: float,
@@ -391,7 +438,7 @@ def derive_edits(topo: GridTopology, original, decompressed, xi: float,
     rc = getattr(lib, f"mssz_cu_derive_edits_{suf}")(
         topo.ndims, _dims(topo), _p(f), _p(fh), C.c_double(xi), C.byref(co), C.byref(idx),
         C.byref(val), C.byref(count), C.byref(st))
-    _check(rc)
+    _check_cb(rc, keep)
     k = count.value
     indices = np.ctypeslib.as_array(idx, shape=(max(k, 1),))[:k].copy()
     values = np.ctypeslib.as_array(val, shape=(max(k, 1),))[:k].copy()
@@ -415,7 +462,7 @@ def derive_edits_into(topo: GridTopology, f_ptr: int, fh_ptr: int, xi: float, id
         topo.ndims, _dims(topo), C.c_void_p(f_ptr), C.c_void_p(fh_ptr), C.c_double(xi),
         C.byref(co), C.c_void_p(idx_ptr), C.c_void_p(val_ptr), C.c_uint64(capacity),
         C.byref(count), C.byref(st))
-    _check(rc)
+    _check_cb(rc, keep)
     return count.value, st.fill(EditStats())
 
 
@@ -432,7 +479,7 @@ def derive_edits_device(topo: GridTopology, d_f: int, d_fh: int, xi: float, d_id
         topo.ndims, _dims(topo), C.c_void_p(d_f), C.c_void_p(d_fh), C.c_double(xi),
         C.byref(co), C.c_void_p(d_idx), C.c_void_p(d_val), C.c_uint64(capacity),
         C.byref(count), C.byref(st), C.c_void_p(stream or None))
-    _check(rc)
+    _check_cb(rc, keep)
     return count.value, st.fill(EditStats())
 
 
@@ -502,6 +549,30 @@ def detect_kind(topo: GridTopology, original, edited, kind: int) -> np.ndarray:
     _check(getattr(library(), f"mssz_cu_detect_kind_{_suf(f.dtype)}")(
         topo.ndims, _dims(topo), _p(f), _p(g), int(kind), _p(out), C.byref(cnt)))
     return out[: cnt.value].copy()
+
+
+@dataclass
+class RBatchTargets:
+    """One R batch's target set (run_r_loop, edit_engine.cpp:336-352)."""
+
+    targets: np.ndarray      # sorted distinct troublemaker targets v_t
+    false_critical: int      # false critical points of (f, g): the R gate (:338)
+    sources: int             # divergent mismatched (vertex, family) pairs = distinct v_i
+    path: str                # "tiled" or "sparse"
+
+
+def r_targets(topo: GridTopology, original, edited, mode: str = "tiled") -> RBatchTargets:
+    """The R-batch targets the engine computes for (f, g): tiled pass or sparse Up(X) pass."""
+    f = _field(topo, original, "original")
+    g = _field(topo, edited, "edited", f.dtype)
+    out = np.empty(topo.vertex_count, np.uint64)
+    cnt = C.c_uint64()
+    info = np.zeros(3, np.uint64)
+    _check(getattr(library(), f"mssz_cu_r_targets_{_suf(f.dtype)}")(
+        topo.ndims, _dims(topo), _p(f), _p(g), {"tiled": 0, "sparse": 1}[mode], _p(out),
+        C.byref(cnt), _p(info)))
+    return RBatchTargets(out[: cnt.value].copy(), int(info[0]), int(info[1]),
+                         "sparse" if info[2] else "tiled")
 
 
 def lower_step(g, f, xi: float):

@@ -27,6 +27,9 @@ namespace mssz_b200 {
 namespace {
 
 thread_local std::string g_last_error;
+// what the current on_batch call reports (mssz_cu_batch_phase): kind, outer
+// iteration, 1-based C pass or R iteration within that outer iteration
+thread_local uint64_t g_phase[3] = {0, 0, 0};
 
 struct Fail {
   int code;
@@ -64,6 +67,9 @@ int guarded(F&& body) {
   } catch (const std::bad_alloc&) {
     g_last_error = "host allocation failed";
     return MSSZ_CU_ERR_CUDA;
+  } catch (...) {  // nothing may unwind through the C ABI
+    g_last_error = "unexpected C++ exception inside the engine";
+    return MSSZ_CU_ERR_INTERNAL;
   }
 }
 
@@ -97,7 +103,11 @@ Geom make_geom(int ndims, const uint64_t* dims) {
     int dx, dy, dz;
     if (ndims == 2) stencil<2>(k, dx, dy, dz);
     else stencil<3>(k, dx, dy, dz);
-    g.off[k] = dx + dy * static_cast<int32_t>(g.X) + dz * static_cast<int32_t>(g.XY);
+    // kernels add offsets in u32 arithmetic (v + off wraps onto the right id for
+    // every in-grid target), so only the value mod 2^32 matters: computed in
+    // int64, stored two's-complement (X + XY + 1 may exceed INT32_MAX)
+    const int64_t o = dx + dy * static_cast<int64_t>(g.X) + dz * static_cast<int64_t>(g.XY);
+    g.off[k] = static_cast<int32_t>(static_cast<uint32_t>(static_cast<uint64_t>(o)));
   }
   return g;
 }
@@ -176,6 +186,8 @@ struct Workspace {
     device = dev;
     CK(cudaSetDevice(dev));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (const char* e = std::getenv("MSSZ_L2_FETCH"))  // experiment: L2 miss fetch granularity
+      CK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, static_cast<size_t>(std::atoi(e))));
     CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
     CK(cudaMalloc(&ctl, sizeof(Ctl)));
@@ -662,12 +674,26 @@ struct Engine {
     return coop_blocks;
   }
 
-  void on_batch() {
+  // per_batch: the device loop stops after every batch (reference call sites);
+  // otherwise on_batch fires only at phase ends (MSSZ_CU_ON_BATCH_PHASES)
+  bool per_batch() const { return opt.on_batch && opt.on_batch_mode == MSSZ_CU_ON_BATCH_EVERY; }
+  uint64_t outer_it = 0, pass_it = 0, r_it = 0;  // phase counters of on_batch
+  uint64_t huge_edits = 0;  // edits of host-driven huge C batches (not k_subloop's)
+  // debug: every subloop skipped as provably empty is re-checked by a full sweep
+  bool check_skips = std::getenv("MSSZ_CHECK_SKIPS") != nullptr;
+  void on_batch(uint64_t kind = MSSZ_CU_PHASE_BATCH) {
     if (!opt.on_batch) return;
+    g_phase[0] = kind;
+    g_phase[1] = outer_it;
+    g_phase[2] = kind == MSSZ_CU_PHASE_R_ITERATION ? r_it : kind == MSSZ_CU_PHASE_C_PASS ? pass_it : pass_it + 1;
     host_g.resize(n());
     CK(cudaMemcpyAsync(host_g.data(), s.g, sizeof(T) * n(), cudaMemcpyDeviceToHost, ws.stream));
     ws.sync();
-    opt.on_batch(host_g.data(), n(), opt.on_batch_user);
+    if (opt.on_batch(host_g.data(), n(), opt.on_batch_user) != 0)
+      fail(MSSZ_CU_ERR_CALLBACK, "on_batch aborted derive_edits");
+  }
+  void on_batch_batch() {  // a fix batch ended
+    if (per_batch()) on_batch();
   }
 
   // One huge batch with streaming kernels (see k_subloop): fix_list, full
@@ -715,17 +741,33 @@ struct Engine {
     c.list_count[cur ^ 1] = 0;
     c.iters += 1;
     c.edits += applied;
+    huge_edits += applied;
     c.frontier += n();
     c.s_count = c.f_count = 0;
     c.status = kStatusOk;
     *ws.hctl = c;
     ws.push_ctl();
-    on_batch();
+    on_batch_batch();
   }
 
   // run_subloop (edit_engine.cpp:246-278)
   uint64_t run_subloop(int kind) {
-    if (fresh[kind] && epoch_end[kind] == code_epoch && !opt.on_batch) return 0;  // list provably empty
+    if (fresh[kind] && epoch_end[kind] == code_epoch && !per_batch()) {  // list provably empty
+      if (check_skips) {  // MSSZ_CHECK_SKIPS: prove it with a full detection sweep
+        reset_ctl();
+        ws.push_ctl();
+        k_detect_kind<<<grid_for((n() + 15) / 16, 256, ws.sms, 16), 256, 0, ws.stream>>>(
+            s.fdir, s.gdir, n(), kind, s.list[cur], &ws.ctl->list_count[cur]);
+        CK_LAUNCH();
+        ws.pull_ctl();
+        if (ws.hctl->list_count[cur])
+          fail(MSSZ_CU_ERR_INTERNAL, "skipped %s subloop has %u items (code epoch invariant broken)",
+               kKindName[kind], ws.hctl->list_count[cur]);
+      }
+      ++st.skipped_subloops;
+      return 0;
+    }
+    const uint64_t huge0 = huge_edits;
     reset_ctl();
     ws.push_ctl();
     const int dcls = fresh[kind] ? kProfDetectDirty : kProfDetectKind;
@@ -750,7 +792,7 @@ struct Engine {
       }
     } id_guard{ws, batch_base, mark_base};
     uint64_t cap = opt.subloop_cap;
-    uint32_t maxb = opt.on_batch ? 1u : 0xFFFFFFFFu;
+    uint32_t maxb = per_batch() ? 1u : 0xFFFFFFFFu;
     uint32_t small_max = kSmallBatchMax;
     uint32_t huge_min = std::max<uint32_t>(kSmallBatchMax, n() / kHugeBatchDivisor);
     uint32_t park_cap = (n() + 63) & ~63u;  // P lives in list(3) (State::F)
@@ -772,7 +814,7 @@ struct Engine {
         seen_iters = ws.hctl->iters;
         continue;
       }
-      if (!opt.on_batch || c.status != kStatusOk) break;
+      if (!per_batch() || c.status != kStatusOk) break;
       if (c.iters == seen_iters) break;  // list empty
       seen_iters = c.iters;
       on_batch();
@@ -795,6 +837,8 @@ struct Engine {
                    c.phase_ns[0] * 1e-6, c.phase_ns[1] * 1e-6, c.phase_ns[2] * 1e-6);
     st.sub_iterations[kind] += c.iters;
     st.effective_edits += c.edits;
+    st.subloop_items += c.items;
+    st.subloop_edits += c.edits - (huge_edits - huge0);
     st.frontier_vertices += c.frontier;
     st.big_batches += c.big_batches;
     if (c.edits) ++code_epoch;
@@ -813,6 +857,8 @@ struct Engine {
         epoch_end[kind] = code_epoch;
       }
       if (pass_edits) r_full_valid = false;  // the tile store no longer matches gdir
+      ++pass_it;
+      if (opt.on_batch && !per_batch()) on_batch(MSSZ_CU_PHASE_C_PASS);  // a C pass ended
       if (pass_edits == 0) return;
     }
   }
@@ -1041,7 +1087,8 @@ struct Engine {
                      (unsigned long long)st.r_iterations, (unsigned long long)mism, ntargets,
                      applied, (unsigned long long)st.label_tiles, (unsigned long long)st.rfix_tiles,
                      1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t_it).count());
-      on_batch();
+      ++r_it;
+      on_batch(MSSZ_CU_PHASE_R_ITERATION);
     }
   }
 
@@ -1104,6 +1151,8 @@ struct Engine {
                                   st.sub_iterations[2] + st.sub_iterations[3]),
              (unsigned long long)st.r_iterations);
       ++st.outer_iterations;
+      outer_it = st.outer_iterations;
+      pass_it = r_it = 0;
       const uint64_t before = st.effective_edits;
       run_c_loop();
       const uint64_t after_c = st.effective_edits;
@@ -1388,6 +1437,50 @@ void detect_host(int ndims, const uint64_t* dims, const T* f, const T* g, int ki
   }
 }
 
+// R-batch target set of run_r_loop (edit_engine.cpp:336-352) for one (f, g)
+// pair: the deduplicated troublemaker targets v_t of every mismatched vertex,
+// through the engine's own tiled pass (k_rfix_tiles -> k_expand_targets) or its
+// sparse Up(X) pass, sorted.  info = {false critical points (the R gate,
+// :338), divergent mismatched (vertex, family) pairs = distinct troublemaker
+// sources v_i, path used (0 tiled, 1 sparse)}.
+template <class T>
+void r_targets_host(int ndims, const uint64_t* dims, const T* f, const T* g, int mode,
+                    uint64_t* targets, uint64_t* count_out, uint64_t* info) {
+  const Geom geo = make_geom(ndims, dims);
+  if (!f || !g || !targets || !count_out || !info) fail(MSSZ_CU_ERR_USAGE, "null pointer");
+  if (mode != 0 && mode != 1) fail(MSSZ_CU_ERR_USAGE, "mode must be 0 (tiled) or 1 (sparse)");
+  mssz_cu_options opt;
+  mssz_cu_default_options(&opt);
+  Workspace& ws = workspace(-1);
+  std::lock_guard<std::mutex> lk(ws.mu);
+  ws.ensure(geo.n, sizeof(T));
+  Engine<T> eng(ws, geo, opt);
+  eng.bind(ws.f.as<T>());
+  CK(cudaMemcpyAsync(ws.f.p, f, sizeof(T) * geo.n, cudaMemcpyHostToDevice, ws.stream));
+  CK(cudaMemcpyAsync(ws.g.p, g, sizeof(T) * geo.n, cudaMemcpyHostToDevice, ws.stream));
+  eng.directions(ws.f.as<T>(), ws.fdir.as<uint8_t>());
+  eng.directions(eng.s.g, eng.s.gdir);
+  eng.label_pass(eng.s.fdir, eng.lab(0), eng.lab(1), false, true);
+  info[0] = eng.count_false_critical();
+  uint64_t mism = 0;
+  int path = 0;
+  if (mode == 1 && eng.sparse_targets(mism)) path = 1;
+  if (path == 0) {
+    eng.label_pass(eng.s.gdir, eng.lab(2), eng.lab(3), false, false);
+    mism = eng.r_targets(true);
+  }
+  const uint32_t nt = ws.hctl->list_count[0];
+  std::vector<uint32_t> t(nt);
+  if (nt) CK(cudaMemcpyAsync(t.data(), eng.list(0), 4ull * nt, cudaMemcpyDeviceToHost, ws.stream));
+  ws.sync();
+  std::sort(t.begin(), t.end());
+  t.erase(std::unique(t.begin(), t.end()), t.end());
+  for (size_t i = 0; i < t.size(); ++i) targets[i] = t[i];
+  *count_out = t.size();
+  info[1] = mism;
+  info[2] = static_cast<uint64_t>(path);
+}
+
 template <class T>
 void elementwise_host(uint64_t n, const T* g, const T* f, double xi, T* out, uint8_t* moved,
                       bool floor_only) {
@@ -1439,17 +1532,46 @@ void apply_host(uint64_t n, const T* fh, const uint64_t* idx, const T* vals, uin
   d.ensure(4);
   CK(cudaMemsetAsync(d.p, 0, 4, ws.stream));
   CK(cudaMemcpyAsync(a.p, fh, sizeof(T) * n, cudaMemcpyHostToDevice, ws.stream));
+  // d = {bad index, indices not non-decreasing}.  The reference applies the
+  // edits in order, so for a repeated index the LAST value wins: with sorted
+  // indices that is the last element of each run (k_scatter), otherwise a
+  // winner pass (atomicMax of position + 1 per vertex) picks it.
+  uint32_t flags[2] = {0, 0};
+  d.ensure(8);
+  CK(cudaMemsetAsync(d.p, 0, 8, ws.stream));
   if (count) {
     CK(cudaMemcpyAsync(b.p, idx, 8 * count, cudaMemcpyHostToDevice, ws.stream));
     CK(cudaMemcpyAsync(c.p, vals, sizeof(T) * count, cudaMemcpyHostToDevice, ws.stream));
-    k_scatter<T><<<grid_for(count, 256, ws.sms, 16), 256, 0, ws.stream>>>(count, b.as<uint64_t>(), c.as<T>(), n, a.as<T>(), d.as<uint32_t>());
+    k_scatter_check<<<grid_for(count, 256, ws.sms, 16), 256, 0, ws.stream>>>(count, b.as<uint64_t>(), n,
+                                                                          d.as<uint32_t>());
     CK_LAUNCH();
+    CK(cudaMemcpyAsync(flags, d.p, 8, cudaMemcpyDeviceToHost, ws.stream));
+    ws.sync();
+    if (flags[0]) fail(MSSZ_CU_ERR_CORRUPT_ARCHIVE, "edit index out of range");  // no output
+    if (!flags[1]) {
+      k_scatter<T><<<grid_for(count, 256, ws.sms, 16), 256, 0, ws.stream>>>(count, b.as<uint64_t>(), c.as<T>(),
+                                                                           a.as<T>());
+      CK_LAUNCH();
+    } else {
+      DevBuf win;
+      struct RelW {
+        DevBuf& w;
+        ~RelW() { w.release(); }
+      } relw{win};
+      win.ensure(8 * (n ? n : 1));
+      CK(cudaMemsetAsync(win.p, 0, 8 * n, ws.stream));
+      k_scatter_winner<<<grid_for(count, 256, ws.sms, 16), 256, 0, ws.stream>>>(count, b.as<uint64_t>(),
+                                                                               win.as<unsigned long long>());
+      k_scatter_won<T><<<grid_for(count, 256, ws.sms, 16), 256, 0, ws.stream>>>(
+          count, b.as<uint64_t>(), c.as<T>(), win.as<unsigned long long>(), a.as<T>());
+      CK_LAUNCH();
+      CK(cudaMemcpyAsync(out, a.p, sizeof(T) * n, cudaMemcpyDeviceToHost, ws.stream));
+      ws.sync();
+      return;
+    }
   }
-  uint32_t bad = 0;
-  CK(cudaMemcpyAsync(&bad, d.p, 4, cudaMemcpyDeviceToHost, ws.stream));
   CK(cudaMemcpyAsync(out, a.p, sizeof(T) * n, cudaMemcpyDeviceToHost, ws.stream));
   ws.sync();
-  if (bad) fail(MSSZ_CU_ERR_CORRUPT_ARCHIVE, "edit index out of range");
 }
 
 void labels_host(int ndims, const uint64_t* dims, const uint64_t* asc, const uint64_t* desc,
@@ -1538,6 +1660,11 @@ void mssz_cu_default_options(mssz_cu_options* o) {
 }
 
 const char* mssz_cu_last_error(void) { return g_last_error.c_str(); }
+int mssz_cu_batch_phase(uint64_t out[3]) {
+  if (!out) return MSSZ_CU_ERR_USAGE;
+  for (int i = 0; i < 3; ++i) out[i] = g_phase[i];
+  return MSSZ_CU_OK;
+}
 void mssz_cu_free(void* p) { std::free(p); }
 const char* mssz_cu_version(void) { return "mssz-b200 0.1 (sm_100a)"; }
 
@@ -1623,6 +1750,10 @@ int mssz_cu_release_workspace(int device) {
   int mssz_cu_apply_edits_##SUF(uint64_t n, const T* fh, const uint64_t* idx, const T* vals,     \
                                 uint64_t count, T* out) {                                         \
     return guarded([&] { apply_host<T>(n, fh, idx, vals, count, out); });                         \
+  }                                                                                               \
+  int mssz_cu_r_targets_##SUF(int ndims, const uint64_t* dims, const T* f, const T* g, int mode, \
+                              uint64_t* targets, uint64_t* count, uint64_t* info) {               \
+    return guarded([&] { r_targets_host<T>(ndims, dims, f, g, mode, targets, count, info); });   \
   }
 
 MSSZ_CU_DEFINE_TYPED(f32, float)

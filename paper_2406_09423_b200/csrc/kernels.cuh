@@ -2437,17 +2437,46 @@ __global__ void k_floor(uint64_t n, const T* __restrict__ f, double xi, T* __res
     out[i] = representable_floor<T>(f[i], xi);
 }
 
-template <class T>
-__global__ void k_scatter(uint64_t count, const uint64_t* __restrict__ idx,
-                          const T* __restrict__ vals, uint64_t n, T* __restrict__ out,
-                          uint32_t* bad) {
+__global__ void k_scatter_check(uint64_t count, const uint64_t* __restrict__ idx, uint64_t n,
+                                uint32_t* flags) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
        i += stride) {
     const uint64_t v = idx[i];
-    if (v >= n) *bad = 1;
-    else out[v] = vals[i];
+    if (v >= n) flags[0] = 1;
+    if (i + 1 < count && idx[i + 1] < v) flags[1] = 1;
   }
+}
+
+// non-decreasing indices: the last element of each run of equal indices wins
+template <class T>
+__global__ void k_scatter(uint64_t count, const uint64_t* __restrict__ idx,
+                          const T* __restrict__ vals, T* __restrict__ out) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += stride) {
+    const uint64_t v = idx[i];
+    if (i + 1 == count || idx[i + 1] != v) out[v] = vals[i];
+  }
+}
+
+// unsorted indices: the largest position per vertex wins (in-order application)
+__global__ void k_scatter_winner(uint64_t count, const uint64_t* __restrict__ idx,
+                                 unsigned long long* __restrict__ win) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += stride)
+    atomicMax(win + idx[i], static_cast<unsigned long long>(i + 1));
+}
+
+template <class T>
+__global__ void k_scatter_won(uint64_t count, const uint64_t* __restrict__ idx,
+                              const T* __restrict__ vals, const unsigned long long* __restrict__ win,
+                              T* __restrict__ out) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += stride)
+    if (win[idx[i]] == i + 1) out[idx[i]] = vals[i];
 }
 
 // dir codes -> the reference's u64 vertex ids (DirectionField, mss.hpp:24-27)
@@ -2460,8 +2489,9 @@ __global__ void k_codes_to_ids(const uint8_t* __restrict__ dir, Geom g, uint64_t
   for (uint64_t v = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < g.n;
        v += stride) {
     const uint32_t c = dir[v];
-    asc[v] = static_cast<uint64_t>(static_cast<int64_t>(v) + off[c & 15u]);
-    desc[v] = static_cast<uint64_t>(static_cast<int64_t>(v) + off[c >> 4]);
+    // u32 wraparound: off holds the stencil offset mod 2^32 (make_geom)
+    asc[v] = static_cast<uint32_t>(v) + static_cast<uint32_t>(off[c & 15u]);
+    desc[v] = static_cast<uint32_t>(v) + static_cast<uint32_t>(off[c >> 4]);
   }
 }
 

@@ -752,7 +752,7 @@ struct SlabEngine {
   uint64_t run_subloop(int kind) {
     // provably empty on every rank (Engine::run_subloop): edit totals, hence
     // the epoch, are global
-    if (eng.fresh[kind] && eng.epoch_end[kind] == eng.code_epoch && !eng.opt.on_batch) return 0;
+    if (eng.fresh[kind] && eng.epoch_end[kind] == eng.code_epoch && !eng.per_batch()) return 0;
     State<T>& S = s();
     uint32_t& cur = eng.cur;
     reset_ctl();

@@ -7,6 +7,7 @@
 #include <cstring>
 #include <string>
 #include <random>
+#include <span>
 #include <vector>
 
 #include "mssz_b200.hpp"
@@ -81,6 +82,26 @@ int main(int argc, char** argv) {
     if (edits.size() && mssz_b200::verified(before)) {
       std::fprintf(stderr, "edits derived although the base reconstruction already verified\n");
       return 1;
+    }
+    // an exception thrown by on_batch propagates out of derive_edits, as in the
+    // reference (edit_engine.cpp:275 calls the std::function inside the loop)
+    {
+      struct Stop {};
+      int calls = 0;
+      mssz_b200::DeriveOptions<float> o2;
+      o2.on_batch = [&](std::span<const float>) {
+        if (++calls == 3) throw Stop{};
+      };
+      bool propagated = false;
+      try {
+        mssz_b200::derive_edits(topo, f.data(), fh.data(), xi, o2);
+      } catch (const Stop&) {
+        propagated = true;
+      }
+      if (!propagated || calls != 3) {
+        std::fprintf(stderr, "on_batch exception did not propagate (calls=%d)\n", calls);
+        return 1;
+      }
     }
     if (argc > 1) {
       const std::string dir = argv[1];

@@ -68,4 +68,4 @@ def test_exported_sizes_in_ctypes(mssz):
     import ctypes as C
     # the ctypes mirrors must have the C layout: 3 u64 + 2 i32 + 2 pointers
     assert C.sizeof(mssz._Options) == 24 + 8 + 16 + 8
-    assert C.sizeof(mssz._Stats) == 8 * 10 + 8 * 5 + 8 * 5 + 56 + 16 * 8 * 2
+    assert C.sizeof(mssz._Stats) == 8 * 10 + 8 * 5 + 8 * 5 + 80 + 16 * 8 * 2

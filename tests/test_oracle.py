@@ -113,3 +113,18 @@ def test_oracle_vs_reference_live(ref_lib, oracle_lib, kind, dims, seed, rel, dt
     for k in ("outer_iterations", "c_passes", "sub_iterations", "r_iterations",
               "effective_edits", "touched"):
         assert r.stats[k] == o.stats[k], k
+
+
+def test_reference_r_targets_troublemaker_kats(golden, ref_lib):
+    """The shim's run_r_loop target collection reproduces the golden (v_i, v_t) of
+    test_edit_engine.cpp:138-185 (the R-batch parity tests compare the GPU with it)."""
+    meta, arr = golden
+    for case in meta["troublemaker"]:
+        f = arr[f"tm/{case['name']}/f"]
+        g = arr[f"tm/{case['name']}/g"]
+        targets, _false, sources, mism = ref_lib.r_targets(case["dims"], f, g)
+        assert case["vt"] in targets.tolist(), case["name"]
+        assert sources >= 1 and mism >= 1
+        vi, vt = ref_lib.find_troublemaker(case["dims"], f, g, case["xi"], case["v"],
+                                           case["descending"])
+        assert (vi, vt) == (case["vi"], case["vt"])
