@@ -125,8 +125,9 @@ def c4(args) -> dict:
     sl = slice(z0 * X * Y, (z0 + args.planes) * X * Y)
     sub_dims = [X, Y, args.planes]
     # kept states: after the first C pass; the state R iteration 1 starts from
-    # (the last C pass before it); the state R iteration 10 of the run starts
-    # from (after R iteration 9); the converged field
+    # (the last C pass before it); after R iterations 1, 10 and 20 of the run
+    # (the start states of the next R batch when the R gate passes there); the
+    # converged field
     snaps: dict = {}
     held = {}
     r_total = [0]
@@ -142,9 +143,9 @@ def c4(args) -> dict:
             if r_total[0] == 1:
                 label, hg = held["last"]
                 snaps[f"{label}: the state R iteration 1 starts from"] = hg
-            if r_total[0] == 9:
-                snaps[f"after R iteration 9 (outer {outer}, #{idx} of its R loop): "
-                      "the state R iteration 10 starts from"] = g
+            if r_total[0] in (1, 10, 20):
+                snaps[f"after R iteration #{r_total[0]} of the run (outer {outer}, #{idx} of "
+                      "its R loop)"] = g
             held.clear()
 
     st = P.EditStats()
