@@ -42,7 +42,9 @@
  *                 points of the pair (the R gate, :338), divergent mismatched
  *                 (vertex, family) pairs = distinct troublemaker sources v_i,
  *                 path used (0 tiled, 1 sparse; mode 1 falls back to 0 when
- *                 Up(X) is too large)}.  Parity harness entry point.
+ *                 Up(X) is too large or the pair has false critical points,
+ *                 where the engine never runs the sparse pass)}.  Parity
+ *                 harness entry point.
  *
  * Conventions (mirroring errors.hpp:9-16): every function returns 0 or the
  * reference ErrKind value (2 usage, 3 io, 4 bound_violation, 5 non_convergence,

@@ -235,7 +235,11 @@ struct Workspace {
     bool fresh = stamp.ensure(np * 4);
     fresh |= fmark.ensure(np * 4);
     lab.ensure(np * 16);    // fM fm gM gm (u32)
-    fin.ensure(np * 8);     // exit finals (finM finm), see k_exit_*
+    // exit finals (finM finm), see k_exit_*.  Zeroed when (re)allocated: an
+    // incremental pass's k_exit_save reads fin at the exits of re-labelled tiles
+    // that may never have been exits before (their saved value only feeds the
+    // change test of a tile that is dirty, hence recomputed, anyway)
+    if (fin.ensure(np * 8)) CK(cudaMemsetAsync(fin.p, 0, fin.cap, stream));
     cbits.ensure((n + 2047) / 2048 * 4 + 4);
     fresh |= cstamp.ensure((n + 63) / 64 * 4 + 4);
     lists.ensure(np * 16);  // list0 list1 S F (u32); reused as the u64+T EditSet
@@ -1464,7 +1468,9 @@ void r_targets_host(int ndims, const uint64_t* dims, const T* f, const T* g, int
   info[0] = eng.count_false_critical();
   uint64_t mism = 0;
   int path = 0;
-  if (mode == 1 && eng.sparse_targets(mism)) path = 1;
+  // the sparse pass assumes the R gate (no false critical points): a g-chain
+  // avoiding X then ends at an f-extremum.  The engine only runs it there.
+  if (mode == 1 && info[0] == 0 && eng.sparse_targets(mism)) path = 1;
   if (path == 0) {
     eng.label_pass(eng.s.gdir, eng.lab(2), eng.lab(3), false, false);
     mism = eng.r_targets(true);

@@ -9,7 +9,7 @@ h = rows[0]
 ik, im, iv, iu, iid = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), \
     h.index("Metric Unit"), h.index("ID")
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
-         "msecond": 1e-3, "second": 1.0, "%": 1.0}
+         "msecond": 1e-3, "second": 1.0, "%": 1.0, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0}
 per = collections.defaultdict(lambda: collections.defaultdict(float))
 launches = collections.defaultdict(set)
 for r in rows[1:]:

@@ -69,6 +69,9 @@ def main() -> None:
             s = P.derive_edits_slabs(topo, f, fh, xi, 3, P.DeriveOptions(subloop_cap=100000))
             assert np.array_equal(s.indices, e.indices) and s.values.tobytes() == e.values.tobytes()
         print(f"  kernels/report/codecs ok", flush=True)
+    # the per-device workspace is a deliberate cache; free it so a leak check
+    # reports only real leaks
+    P.library().mssz_cu_release_workspace(-1)
     print("sanitize cases ok")
 
 
