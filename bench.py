@@ -459,9 +459,26 @@ def main():
                 gbs = ent["dram_bytes_per_launch"] / dur / 1e9
                 dominant.update({"bound": "hbm (random 32 B sectors)", "dram_GBps_ncu": gbs,
                                  "frac_of_peak": gbs / peak, "source": "profiles/ncu_traffic_c4.json"})
+        # random-access view (profiles/r02_random_gather_peak.json): a scattered
+        # 4-byte access moves ~128 B of DRAM traffic on this B200, and random
+        # reads saturate at ~37.8 G accesses/s; the graded kernel's DRAM traffic
+        # (ncu) / bytes-per-access / its launch time against that ceiling
+        random_access = None
+        rpath = os.path.join(ROOT, "profiles", "r02_random_gather_peak.json")
+        if traffic and os.path.exists(rpath):
+            with open(rpath) as fp:
+                rp = json.load(fp)
+            bpa = statistics.mean(v for k, v in rp["ncu_dram_bytes_per_access"].items() if ", 0>" in k)
+            acc_s = traffic / bpa / (per_launch_ms * 1e-3)
+            random_access = {"achieved_Gaccess_s": acc_s / 1e9,
+                             "peak_Gaccess_s": rp["random_read_ceiling_Gaccess_s"],
+                             "frac": acc_s / 1e9 / rp["random_read_ceiling_Gaccess_s"],
+                             "dram_bytes_per_access": bpa,
+                             "source": "profiles/r02_random_gather_peak.json (tools/random_gather_peak.cu)"}
         roofline = {"kernel": top, "bound": "hbm", "achieved": achieved, "peak": peak,
                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                     "dram_over_algorithmic": (traffic / bytes_per_launch) if traffic else None,
+                    "random_access": random_access,
                     "peak_source": peak_src,
                     "alg_bytes_per_launch": bytes_per_launch,
                     "mean_launch_us": per_launch_ms * 1e3,

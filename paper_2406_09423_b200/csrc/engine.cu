@@ -193,9 +193,13 @@ struct Workspace {
     CK(cudaMalloc(&ctl, sizeof(Ctl)));
     CK(cudaMallocHost(&hctl, sizeof(Ctl)));
     for (auto& e : ev) CK(cudaEventCreate(&e));
-    CK(cudaFuncSetAttribute(k_label_tile<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(k_label_tile<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(label_tile_smem<2>())));
-    CK(cudaFuncSetAttribute(k_label_tile<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(k_label_tile<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(label_tile_smem<3>())));
+    CK(cudaFuncSetAttribute(k_label_tile<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(label_tile_smem<2>())));
+    CK(cudaFuncSetAttribute(k_label_tile<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(label_tile_smem<3>())));
     CK(cudaFuncSetAttribute(k_directions_reg3<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(sizeof(D3Smem))));
@@ -554,12 +558,21 @@ struct Engine {
     }
     if (ntodo) {
       pre(kProfLabelInit);
-      if (geo.ndims == 2)
-        k_label_tile<2><<<ntodo, kLabelTileThreads, label_tile_smem<2>(), ws.stream>>>(
-            dir, geo, M, m, fM, fm, list, ts);
-      else
-        k_label_tile<3><<<ntodo, kLabelTileThreads, label_tile_smem<3>(), ws.stream>>>(
-            dir, geo, M, m, fM, fm, list, ts);
+      if (geo.ndims == 2) {
+        if (label_skip)
+          k_label_tile<2, true><<<ntodo, kLabelTileThreads, label_tile_smem<2>(), ws.stream>>>(
+              dir, geo, M, m, fM, fm, list, ts);
+        else
+          k_label_tile<2, false><<<ntodo, kLabelTileThreads, label_tile_smem<2>(), ws.stream>>>(
+              dir, geo, M, m, fM, fm, list, ts);
+      } else {
+        if (label_skip)
+          k_label_tile<3, true><<<ntodo, kLabelTileThreads, label_tile_smem<3>(), ws.stream>>>(
+              dir, geo, M, m, fM, fm, list, ts);
+        else
+          k_label_tile<3, false><<<ntodo, kLabelTileThreads, label_tile_smem<3>(), ws.stream>>>(
+              dir, geo, M, m, fM, fm, list, ts);
+      }
       launched(kProfLabelInit);
     }
     st.label_tiles += ntodo;
@@ -685,6 +698,8 @@ struct Engine {
   uint64_t huge_edits = 0;  // edits of host-driven huge C batches (not k_subloop's)
   // debug: every subloop skipped as provably empty is re-checked by a full sweep
   bool check_skips = std::getenv("MSSZ_CHECK_SKIPS") != nullptr;
+  // k_label_tile: drop settled pointer slots per warp (MSSZ_LABEL_SKIP=0: off)
+  bool label_skip = !std::getenv("MSSZ_LABEL_SKIP") || std::atoi(std::getenv("MSSZ_LABEL_SKIP")) != 0;
   void on_batch(uint64_t kind = MSSZ_CU_PHASE_BATCH) {
     if (!opt.on_batch) return;
     g_phase[0] = kind;
