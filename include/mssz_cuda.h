@@ -34,7 +34,9 @@
  *                 wins); an out-of-range index fails with corrupt_archive and
  *                 writes no output.
  *   mssz_cu_r_targets_{f32,f64}
- *       one R-loop batch's target set (run_r_loop, edit_engine.cpp:336-352:
+ *       one R-loop batch's target set behind the R gate (a pair with false
+ *                 critical points returns 0 targets, as run_r_loop returns at
+ *                 edit_engine.cpp:338) (run_r_loop, edit_engine.cpp:336-352:
  *                 collect_mismatched + find_troublemaker :293-315 + claim) for an
  *                 (original, edited) pair, computed by the engine's tiled pass
  *                 (mode 0) or its sparse Up(X) pass (mode 1).  targets: caller
@@ -42,9 +44,7 @@
  *                 points of the pair (the R gate, :338), divergent mismatched
  *                 (vertex, family) pairs = distinct troublemaker sources v_i,
  *                 path used (0 tiled, 1 sparse; mode 1 falls back to 0 when
- *                 Up(X) is too large or the pair has false critical points,
- *                 where the engine never runs the sparse pass)}.  Parity
- *                 harness entry point.
+ *                 Up(X) is too large)}.  Parity harness entry point.
  *
  * Conventions (mirroring errors.hpp:9-16): every function returns 0 or the
  * reference ErrKind value (2 usage, 3 io, 4 bound_violation, 5 non_convergence,

@@ -233,8 +233,8 @@ namespace {
 // collect_mismatched, find_troublemaker per mismatched vertex and family; the
 // claim dedupe becomes sort + unique.  info = {false critical points of (f, g)
 // (the gate, :338), distinct (v_i, family) troublemaker sources, mismatched
-// vertices}.  The gate is reported, not applied, so a caller can also ask for
-// targets of a state the loop would hand back to the C-loop.
+// vertices}.  Behind the gate only: a pair with false critical points has no
+// R batch (run_r_loop returns there), so its target set is empty.
 template <class T>
 int r_targets_impl(int ndims, const uint64_t* dims, const T* f, const T* g, int threads,
                    uint64_t* targets, uint64_t* count, uint64_t* info) {
@@ -243,6 +243,11 @@ int r_targets_impl(int ndims, const uint64_t* dims, const T* f, const T* g, int 
     EditState<T> state(topo, f, g, 1.0, make_policy(threads));
     state.refresh_directions();
     info[0] = state.detect_false_critical().total();
+    if (info[0] != 0) {  // the gate (edit_engine.cpp:338): no R batch
+      info[1] = info[2] = 0;
+      *count = 0;
+      return;
+    }
     EditEngineTestAccess::compute_g_labels(state);
     std::vector<VertexId> mismatched;
     info[2] = EditEngineTestAccess::collect_mismatched(state, mismatched);

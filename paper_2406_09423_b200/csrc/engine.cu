@@ -193,13 +193,9 @@ struct Workspace {
     CK(cudaMalloc(&ctl, sizeof(Ctl)));
     CK(cudaMallocHost(&hctl, sizeof(Ctl)));
     for (auto& e : ev) CK(cudaEventCreate(&e));
-    CK(cudaFuncSetAttribute(k_label_tile<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(k_label_tile<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(label_tile_smem<2>())));
-    CK(cudaFuncSetAttribute(k_label_tile<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(label_tile_smem<3>())));
-    CK(cudaFuncSetAttribute(k_label_tile<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(label_tile_smem<2>())));
-    CK(cudaFuncSetAttribute(k_label_tile<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(k_label_tile<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(label_tile_smem<3>())));
     CK(cudaFuncSetAttribute(k_directions_reg3<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(sizeof(D3Smem))));
@@ -525,6 +521,7 @@ struct Engine {
     t.mis_cnt = ws.tcnt.as<uint32_t>();
     t.own_lo = s.own_n ? s.own_lo : 0u;
     t.own_hi = s.own_n ? s.own_lo + s.own_n : n();
+    t.err = &ws.ctl->flags[63];
     return t;
   }
   uint32_t* tile_list(int k) const { return ws.tlist.as<uint32_t>() + size_t(k) * label_tiles(); }
@@ -557,22 +554,14 @@ struct Engine {
       list = tile_list(0);
     }
     if (ntodo) {
+      CK(cudaMemsetAsync(ts.err, 0, sizeof(uint32_t), ws.stream));
       pre(kProfLabelInit);
-      if (geo.ndims == 2) {
-        if (label_skip)
-          k_label_tile<2, true><<<ntodo, kLabelTileThreads, label_tile_smem<2>(), ws.stream>>>(
-              dir, geo, M, m, fM, fm, list, ts);
-        else
-          k_label_tile<2, false><<<ntodo, kLabelTileThreads, label_tile_smem<2>(), ws.stream>>>(
-              dir, geo, M, m, fM, fm, list, ts);
-      } else {
-        if (label_skip)
-          k_label_tile<3, true><<<ntodo, kLabelTileThreads, label_tile_smem<3>(), ws.stream>>>(
-              dir, geo, M, m, fM, fm, list, ts);
-        else
-          k_label_tile<3, false><<<ntodo, kLabelTileThreads, label_tile_smem<3>(), ws.stream>>>(
-              dir, geo, M, m, fM, fm, list, ts);
-      }
+      if (geo.ndims == 2)
+        k_label_tile<2><<<ntodo, kLabelTileThreads, label_tile_smem<2>(), ws.stream>>>(
+            dir, geo, M, m, fM, fm, list, ts);
+      else
+        k_label_tile<3><<<ntodo, kLabelTileThreads, label_tile_smem<3>(), ws.stream>>>(
+            dir, geo, M, m, fM, fm, list, ts);
       launched(kProfLabelInit);
     }
     st.label_tiles += ntodo;
@@ -611,10 +600,11 @@ struct Engine {
       k_exit_changed<<<ts.ntiles, 256, 0, ws.stream>>>(ts, fM, fm);
       launched(kProfLabelJump);
     }
-    uint32_t left[2];
+    uint32_t left[2], tile_err = 0;
     CK(cudaMemcpyAsync(left, cnt[rounds & 1], sizeof left, cudaMemcpyDeviceToHost, ws.stream));
+    if (ntodo) CK(cudaMemcpyAsync(&tile_err, ts.err, sizeof tile_err, cudaMemcpyDeviceToHost, ws.stream));
     ws.sync();
-    if (left[0] || left[1])
+    if (left[0] || left[1] || tile_err)
       fail(MSSZ_CU_ERR_INTERNAL, "path compression exceeded its round cap (corrupt direction field)");
     if (finish) {
       pre(kProfLabelFinish);
@@ -698,8 +688,6 @@ struct Engine {
   uint64_t huge_edits = 0;  // edits of host-driven huge C batches (not k_subloop's)
   // debug: every subloop skipped as provably empty is re-checked by a full sweep
   bool check_skips = std::getenv("MSSZ_CHECK_SKIPS") != nullptr;
-  // k_label_tile: drop settled pointer slots per warp (MSSZ_LABEL_SKIP=0: off)
-  bool label_skip = !std::getenv("MSSZ_LABEL_SKIP") || std::atoi(std::getenv("MSSZ_LABEL_SKIP")) != 0;
   void on_batch(uint64_t kind = MSSZ_CU_PHASE_BATCH) {
     if (!opt.on_batch) return;
     g_phase[0] = kind;
@@ -1457,7 +1445,8 @@ void detect_host(int ndims, const uint64_t* dims, const T* f, const T* g, int ki
 }
 
 // R-batch target set of run_r_loop (edit_engine.cpp:336-352) for one (f, g)
-// pair: the deduplicated troublemaker targets v_t of every mismatched vertex,
+// pair behind the R gate (:338; a pair with false critical points has no R
+// batch): the deduplicated troublemaker targets v_t of every mismatched vertex,
 // through the engine's own tiled pass (k_rfix_tiles -> k_expand_targets) or its
 // sparse Up(X) pass, sorted.  info = {false critical points (the R gate,
 // :338), divergent mismatched (vertex, family) pairs = distinct troublemaker
@@ -1481,11 +1470,15 @@ void r_targets_host(int ndims, const uint64_t* dims, const T* f, const T* g, int
   eng.directions(eng.s.g, eng.s.gdir);
   eng.label_pass(eng.s.fdir, eng.lab(0), eng.lab(1), false, true);
   info[0] = eng.count_false_critical();
+  if (info[0] != 0) {  // the R gate (edit_engine.cpp:338): run_r_loop hands back to the C loop
+    *count_out = 0;
+    info[1] = 0;
+    info[2] = 0;
+    return;
+  }
   uint64_t mism = 0;
   int path = 0;
-  // the sparse pass assumes the R gate (no false critical points): a g-chain
-  // avoiding X then ends at an f-extremum.  The engine only runs it there.
-  if (mode == 1 && info[0] == 0 && eng.sparse_targets(mism)) path = 1;
+  if (mode == 1 && eng.sparse_targets(mism)) path = 1;
   if (path == 0) {
     eng.label_pass(eng.s.gdir, eng.lab(2), eng.lab(3), false, false);
     mism = eng.r_targets(true);

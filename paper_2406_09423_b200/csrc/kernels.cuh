@@ -1418,13 +1418,14 @@ struct TileStore {
   // vertices outside [own_lo, own_hi) are labelled as extrema (z-slab windows:
   // chains stop at their first off-slab vertex); single device: the whole grid
   uint32_t own_lo, own_hi;
+  uint32_t* err;  // set when in-tile doubling exceeds its round cap (a cycle)
 };
 
 // Phase 1.  Writes the provisional label (root, or first vertex outside the
 // tile) to prov, fin[r] = r at roots, and the tile's distinct exits to the
 // tile store.
 // tile_list == nullptr: CTA i handles tile i.
-template <int DIM, bool kSkip = true>
+template <int DIM>
 __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
     const uint8_t* __restrict__ dir, Geom g, uint32_t* __restrict__ M, uint32_t* __restrict__ m,
     uint32_t* __restrict__ finM, uint32_t* __restrict__ finm, const uint32_t* tile_list,
@@ -1530,38 +1531,34 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
     const uint2 e = scode[code];  // SELF: offset 0, no face
     const uint32_t pa = (e.y & on) ? i : i + static_cast<int32_t>(static_cast<int16_t>(e.x & 0xFFFFu));
     const uint32_t pd = ((e.y >> 8) & on) ? i : i + (static_cast<int32_t>(e.x) >> 16);
-    // byte offsets into ptr (index * 4 < 2^15): the doubling loads address
-    // shared memory with the packed halves directly
-    own[j] = (pa << 2) | (pd << 18);
+    own[j] = pa | (pd << 16);
     ptr[i] = own[j];
   }
   __syncthreads();
   // in-place doubling on both families at once; a thread's own pointers live
   // in registers (only this thread writes them), the others are read from smem.
-  // A pointer pair that stopped changing points at two fixpoints (roots or
-  // tile exits stop at themselves) and never changes again: `live` drops it,
-  // and a warp skips slot j once none of its lanes has slot j live.
-  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
-  uint32_t live = (1u << PER) - 1u;
-  for (;;) {
-    const uint32_t wlive = kSkip ? __reduce_or_sync(0xffffffffu, live) : 0xFFFFFFFFu;  // warp-uniform
+  // Chains inside a tile are shorter than kLabelTileN, so an acyclic field
+  // settles within bit_width(kLabelTileN) + 1 rounds; a cyclic (corrupt)
+  // direction field would never settle: capped, flagged, raised by the host
+  // like the reference's round cap (mss.cpp:60-80).
+  for (int round = 0;; ++round) {
+    if (round > 2 * 14 + 4) {
+      if (threadIdx.x == 0 && ts.err) atomicExch(ts.err, 1u);
+      break;
+    }
+    bool changed = false;
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
-      if (!(wlive & (1u << j))) continue;
+      const int i = threadIdx.x + j * kLabelTileThreads;
       const uint32_t p = own[j];
-      uint32_t a, d;
-      asm volatile("ld.shared.u16 %0, [%1];" : "=r"(a) : "r"(sbase + (p & 0xFFFFu)));
-      asm volatile("ld.shared.u16 %0, [%1+2];" : "=r"(d) : "r"(sbase + (p >> 16)));
-      const uint32_t np = a | (d << 16);
+      const uint32_t np = (ptr[p & 0xFFFFu] & 0xFFFFu) | (ptr[p >> 16] & 0xFFFF0000u);
       if (np != p) {
         own[j] = np;
-        asm volatile("st.shared.u32 [%0], %1;" ::"r"(sbase + 4u * (threadIdx.x + j * kLabelTileThreads)),
-                     "r"(np));
-      } else {
-        live &= ~(1u << j);
+        ptr[i] = np;
+        changed = true;
       }
     }
-    if (!__syncthreads_or(live != 0u)) break;
+    if (!__syncthreads_or(changed)) break;
   }
   // provisional labels (root, or first vertex outside the tile) + the exits:
   // the chain's last inside vertex t is a root (code SELF) or steps out by
@@ -1575,7 +1572,7 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
       const uint32_t gi = base + lx + g.X * ly + g.XY * lz;
 #pragma unroll
       for (int fam = 0; fam < 2; ++fam) {
-        const int t = (fam ? (p >> 16) : (p & 0xFFFFu)) >> 2;
+        const int t = fam ? (p >> 16) : (p & 0xFFFFu);
         const uint32_t c = (sdir[t] >> (4 * fam)) & 15u;
         const uint32_t res = base + (t & (TL::TX - 1)) + g.X * ((t >> TL::LX) & (TL::TY - 1)) +
                              g.XY * (t >> (TL::LX + TL::LY)) + soff[c];
