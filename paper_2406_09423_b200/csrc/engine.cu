@@ -975,6 +975,7 @@ struct Engine {
       uint32_t mk = mark, mu = max_up, ml = kSparseMaxLevels;
       Ctl* ctl = ws.ctl;
       void* args[] = {(void*)&gd, &gg, &fam, &fmk, &mk, &fa, &fb, &up, &mu, &ml, &ctl};
+      if (trace) std::fprintf(stderr, "[mssz] sparse fam=%d nx=%u: k_upstream blocks=%d occ=%d\n", fam, nx, blocks, occ);
       pre(kProfSparse);
       CK(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(512), args, 0, ws.stream));
       launched(kProfSparse);
@@ -1002,6 +1003,7 @@ struct Engine {
         uint32_t flags[4];
         CK(cudaMemcpyAsync(flags, ws.ctl->flags, sizeof flags, cudaMemcpyDeviceToHost, ws.stream));
         ws.sync();
+        if (trace) std::fprintf(stderr, "[mssz] sparse fam=%d jump round %d flags %u%u%u%u\n", fam, round, flags[0], flags[1], flags[2], flags[3]);
         if (!flags[3]) break;
         if (round > 70) fail(MSSZ_CU_ERR_INTERNAL, "integral line cycle in the sparse R pass");
       }
@@ -1466,10 +1468,20 @@ void r_targets_host(int ndims, const uint64_t* dims, const T* f, const T* g, int
   eng.bind(ws.f.as<T>());
   CK(cudaMemcpyAsync(ws.f.p, f, sizeof(T) * geo.n, cudaMemcpyHostToDevice, ws.stream));
   CK(cudaMemcpyAsync(ws.g.p, g, sizeof(T) * geo.n, cudaMemcpyHostToDevice, ws.stream));
+  auto tr = [&](const char* what) {
+    if (eng.trace) {
+      CK(cudaStreamSynchronize(ws.stream));
+      std::fprintf(stderr, "[mssz] r_targets mode=%d n=%u: %s\n", mode, geo.n, what);
+    }
+  };
+  tr("start");
   eng.directions(ws.f.as<T>(), ws.fdir.as<uint8_t>());
   eng.directions(eng.s.g, eng.s.gdir);
+  tr("directions");
   eng.label_pass(eng.s.fdir, eng.lab(0), eng.lab(1), false, true);
+  tr("f labels");
   info[0] = eng.count_false_critical();
+  tr("gate");
   if (info[0] != 0) {  // the R gate (edit_engine.cpp:338): run_r_loop hands back to the C loop
     *count_out = 0;
     info[1] = 0;
@@ -1479,9 +1491,12 @@ void r_targets_host(int ndims, const uint64_t* dims, const T* f, const T* g, int
   uint64_t mism = 0;
   int path = 0;
   if (mode == 1 && eng.sparse_targets(mism)) path = 1;
+  tr(path ? "sparse done" : "sparse skipped");
   if (path == 0) {
     eng.label_pass(eng.s.gdir, eng.lab(2), eng.lab(3), false, false);
+    tr("g labels");
     mism = eng.r_targets(true);
+    tr("tiled targets");
   }
   const uint32_t nt = ws.hctl->list_count[0];
   std::vector<uint32_t> t(nt);

@@ -2074,10 +2074,17 @@ __global__ void __launch_bounds__(512, 2)
   uint32_t* cnt = ctl->sp_count;  // [1], [2]: frontier sizes; [3]: |Up|
   int cur = 0;
   uint32_t levels = 0;
+  // Every exit decision must be identical in all threads (a thread that leaves
+  // while others wait in grid.sync deadlocks the grid).  The frontier size and
+  // the abort word are written only between the two grid barriers of a level,
+  // so the reads at the top of the next level are stable; |Up| (cnt[3]) keeps
+  // growing while fast warps already append the next level, so it is compared
+  // with max_up by thread 0 between the barriers, never at the top.
   for (;;) {
     const uint32_t n = *reinterpret_cast<volatile uint32_t*>(&cnt[1 + cur]);
     if (n == 0) break;
-    if (*reinterpret_cast<volatile uint32_t*>(&cnt[3]) > max_up || levels >= max_levels) {
+    if (*reinterpret_cast<volatile uint32_t*>(&ctl->sp_abort)) break;
+    if (levels >= max_levels) {
       if (tid == 0) ctl->sp_abort = 1;
       break;
     }
@@ -2111,7 +2118,10 @@ __global__ void __launch_bounds__(512, 2)
       warp_append_cap(mine, u, up, &cnt[3], max_up);
     }
     grid.sync();
-    if (tid == 0) cnt[1 + cur] = 0;
+    if (tid == 0) {
+      cnt[1 + cur] = 0;
+      if (*reinterpret_cast<volatile uint32_t*>(&cnt[3]) > max_up) ctl->sp_abort = 1;
+    }
     cur ^= 1;
     ++levels;
     grid.sync();
