@@ -384,6 +384,7 @@ struct Engine {
     s.F = list(3);
     s.fM = lab(0);
     s.fm = lab(1);
+    s.fM64 = s.fm64 = nullptr;
     s.gM = lab(2);
     s.gm = lab(3);
     s.xi = 0;

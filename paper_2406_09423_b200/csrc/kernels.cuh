@@ -96,14 +96,17 @@ __device__ __forceinline__ int slab_owner(const SlabTable& t, uint32_t z) {
 
 // Slot of global vertex L in the gathered label table [rank][family][side][xy],
 // or -1 when L is not on the first (side 0) or last (side 1) plane of its slab.
-__device__ __forceinline__ int64_t table_slot(const SlabTable& t, uint32_t L, int fam) {
-  const uint32_t z = L / t.XY;
+// Global ids are u64 (a sharded field may exceed 2^32 vertices; the reference
+// caps grids at 2^40, grid.cpp:19); planes and window-local ids stay u32.
+__device__ __forceinline__ int64_t table_slot(const SlabTable& t, uint64_t L, int fam) {
+  const uint32_t z = static_cast<uint32_t>(L / t.XY);
   const int r = slab_owner(t, z);
   int side;
   if (z == t.z0[r]) side = 0;
   else if (z + 1 == t.z0[r + 1]) side = 1;
   else return -1;
-  return ((static_cast<int64_t>(r) * 2 + fam) * 2 + side) * t.XY + (L - z * t.XY);
+  return ((static_cast<int64_t>(r) * 2 + fam) * 2 + side) * t.XY +
+         static_cast<int64_t>(L - static_cast<uint64_t>(z) * t.XY);
 }
 
 // R target slot a rank does not own (z-slab windows): fix_batch's ownership test
@@ -114,13 +117,13 @@ constexpr uint32_t kNoTarget = 0xFFFFFFFFu;
 // label lying on a slab boundary plane is replaced by its resolved table entry.
 // tab == nullptr on a single device (labels are already final).
 struct SlabRes {
-  const uint32_t* tab;
+  const uint64_t* tab;
   SlabTable t;
-  uint32_t base;  // global id of window vertex 0
+  uint64_t base;  // global id of window vertex 0
 };
-__device__ __forceinline__ uint32_t resolve_label(const SlabRes& r, uint32_t local, int fam) {
-  if (!r.tab) return local;
-  const uint32_t L = local + r.base;
+__device__ __forceinline__ uint64_t resolve_label(const SlabRes& r, uint32_t local, int fam) {
+  if (!r.tab) return local + r.base;  // single device / one slab: base of the window (0 on a device)
+  const uint64_t L = local + r.base;
   const int64_t sl = table_slot(r.t, L, fam);
   return sl >= 0 ? __ldg(r.tab + sl) : L;
 }
@@ -688,6 +691,10 @@ struct State {
   const uint32_t* fm;
   const uint32_t* gM;
   const uint32_t* gm;
+  // z-slab windows: final f labels as u64 global ids (nullptr on a single device,
+  // where fM / fm are the final labels)
+  const uint64_t* fM64;
+  const uint64_t* fm64;
   double xi;
   Ctl* ctl;
   uint8_t* tdirty;  // R-loop only: label tiles whose direction codes changed
@@ -1881,14 +1888,15 @@ __global__ void __launch_bounds__(256) k_rfix_tiles(State<T> s, const uint32_t* 
       const uint32_t fc = __ldg(s.fdir + v), gc = __ldg(s.gdir + v);
       const bool wa = (gc & 15u) != (fc & 15u);  // ascending line diverges at v
       const bool wd = (gc >> 4) != (fc >> 4);    // descending line diverges at v
-      uint32_t la = 0, ld = 0, fa = 0, fd = 0;
+      uint32_t la = 0, ld = 0;
+      uint64_t fa = 0, fd = 0;
       if (wa) {
         la = __ldg(s.gM + v);
-        fa = __ldg(s.fM + v);
+        fa = s.fM64 ? __ldg(s.fM64 + v) : __ldg(s.fM + v);
       }
       if (wd) {
         ld = __ldg(s.gm + v);
-        fd = __ldg(s.fm + v);
+        fd = s.fm64 ? __ldg(s.fm64 + v) : __ldg(s.fm + v);
       }
       ma = wa && resolve_label(sr, __ldg(finM + la), 0) != fa;
       md = wd && resolve_label(sr, __ldg(finm + ld), 1) != fd;

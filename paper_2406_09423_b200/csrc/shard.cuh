@@ -49,7 +49,7 @@ namespace {
 // (global id, lowered value) of a boundary target.
 template <class T>
 struct BEdit {
-  uint32_t idx;
+  uint64_t idx;
   T val;
 };
 
@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(256) k_unpark_merge(const uint32_t* __restrict
 // planes -> (global id, value) for the neighbour below / above.
 template <class T>
 __global__ void __launch_bounds__(256) k_pack_boundary(State<T> s, uint32_t lo_end, uint32_t hi_begin,
-                                                       int has_lo, int has_hi, uint32_t base,
+                                                       int has_lo, int has_hi, uint64_t base,
                                                        BEdit<T>* __restrict__ to_lo,
                                                        BEdit<T>* __restrict__ to_hi) {
   const uint32_t n = s.ctl->s_count;
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(256) k_pack_boundary(State<T> s, uint32_t lo_e
 template <class T>
 __global__ void __launch_bounds__(256) k_unpack_boundary(State<T> s, const BEdit<T>* __restrict__ a,
                                                          uint32_t na, const BEdit<T>* __restrict__ b,
-                                                         uint32_t nb, uint32_t base) {
+                                                         uint32_t nb, uint64_t base) {
   const uint64_t n = static_cast<uint64_t>(na) + nb;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t wb = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) & ~uint64_t(31);
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(256) k_unpack_boundary(State<T> s, const BEdit
     uint32_t v = 0;
     if (i < n) {
       const BEdit<T> e = i < na ? a[i] : b[i - na];
-      v = e.idx - base;
+      v = static_cast<uint32_t>(e.idx - base);
       s.g[v] = e.val;
     }
     const uint32_t p = warp_reserve(i < n ? 1u : 0u, &s.ctl->s_count);
@@ -274,8 +274,8 @@ __global__ void __launch_bounds__(256) k_publish_labels(const uint32_t* __restri
                                                         const uint32_t* __restrict__ m,
                                                         const uint32_t* __restrict__ finM,
                                                         const uint32_t* __restrict__ finm, uint32_t XY,
-                                                        uint32_t own_lo, uint32_t own_hi, uint32_t base,
-                                                        uint32_t* __restrict__ tab) {
+                                                        uint32_t own_lo, uint32_t own_hi, uint64_t base,
+                                                        uint64_t* __restrict__ tab) {
   const uint64_t total = 4ull * XY;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(256) k_publish_labels(const uint32_t* __restri
     const int side = static_cast<int>((i / XY) & 1);
     const uint32_t xy = static_cast<uint32_t>(i % XY);
     const uint32_t v = side ? own_hi - XY + xy : own_lo + xy;
-    tab[i] = (fam ? finm[m[v]] : finM[M[v]]) + base;
+    tab[i] = static_cast<uint64_t>(fam ? finm[m[v]] : finM[M[v]]) + base;
   }
 }
 
@@ -292,19 +292,19 @@ __global__ void __launch_bounds__(256) k_publish_labels(const uint32_t* __restri
 // itself (a boundary extremum).  Chasing writes every intermediate back, so
 // concurrent chasers shorten each other's paths; any value written is an
 // ancestor on the same chain, so the fixpoint is the unique terminus.
-__global__ void __launch_bounds__(256) k_resolve_table(uint32_t* __restrict__ tab, SlabTable t,
+__global__ void __launch_bounds__(256) k_resolve_table(uint64_t* __restrict__ tab, SlabTable t,
                                                        uint32_t* err) {
   const uint64_t total = static_cast<uint64_t>(t.P) * 4 * t.XY;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
     const int fam = static_cast<int>((e / (2ull * t.XY)) & 1);
-    volatile uint32_t* vt = tab;
-    uint32_t L = vt[e];
+    volatile uint64_t* vt = tab;
+    uint64_t L = vt[e];
     uint64_t hops = 0;
     for (;;) {
       const int64_t sl = table_slot(t, L, fam);
       if (sl < 0) break;
-      const uint32_t L2 = vt[sl];
+      const uint64_t L2 = vt[sl];
       if (L2 == L) break;
       L = L2;
       if (++hops > total) {  // a cycle: corrupt direction field
@@ -322,13 +322,13 @@ __global__ void __launch_bounds__(256) k_final_labels(const uint32_t* __restrict
                                                       const uint32_t* __restrict__ m,
                                                       const uint32_t* __restrict__ finM,
                                                       const uint32_t* __restrict__ finm,
-                                                      const uint32_t* __restrict__ tab, SlabTable t,
-                                                      uint32_t lo, uint32_t hi, uint32_t base,
-                                                      int resolve, uint32_t* __restrict__ FM,
-                                                      uint32_t* __restrict__ Fm) {
+                                                      const uint64_t* __restrict__ tab, SlabTable t,
+                                                      uint32_t lo, uint32_t hi, uint64_t base,
+                                                      int resolve, uint64_t* __restrict__ FM,
+                                                      uint64_t* __restrict__ Fm) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t v = lo + static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < hi; v += stride) {
-    uint32_t a = finM[M[v]] + base, d = finm[m[v]] + base;
+    uint64_t a = finM[M[v]] + base, d = finm[m[v]] + base;
     if (resolve) {
       const int64_t sa = table_slot(t, a, 0), sd = table_slot(t, d, 1);
       if (sa >= 0) a = __ldg(tab + sa);
@@ -341,13 +341,13 @@ __global__ void __launch_bounds__(256) k_final_labels(const uint32_t* __restrict
 
 // Boundary-table entries that changed since the previous R iteration (the
 // resolved table is then kept as the reference for the next one).
-__global__ void __launch_bounds__(256) k_table_diff(const uint32_t* __restrict__ tab, uint32_t* __restrict__ prev,
+__global__ void __launch_bounds__(256) k_table_diff(const uint64_t* __restrict__ tab, uint64_t* __restrict__ prev,
                                                     uint8_t* __restrict__ changed, uint64_t total,
                                                     uint32_t* any) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   bool c_any = false;
   for (uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
-    const uint32_t a = tab[e];
+    const uint64_t a = tab[e];
     const bool c = a != prev[e];
     changed[e] = c ? 1 : 0;
     if (c) {
@@ -366,7 +366,7 @@ template <int DIM>
 __global__ void __launch_bounds__(256) k_slab_affected(TileStore ts, const uint32_t* __restrict__ finM,
                                                        const uint32_t* __restrict__ finm,
                                                        const uint8_t* __restrict__ changed, const uint32_t* any,
-                                                       SlabTable t, Geom g, uint32_t base) {
+                                                       SlabTable t, Geom g, uint64_t base) {
   using TL = LabelTile<DIM>;
   if (!*any) return;
   const uint32_t b = blockIdx.x;
@@ -599,10 +599,11 @@ SlabPlan slab_plan(uint64_t Z, int P, int r) {
 // Workspace extras of the sharded loop.
 struct SlabBufs {
   DevBuf tab_mine, tab_all, tab_prev, tchanged, send[2], recv[2], rec, rec_all;
+  DevBuf flab;   // final f labels of the window as u64 global ids (FM | Fm)
   DevBuf flags;  // [0] table resolution hit a cycle, [1] a table entry changed
   std::vector<Rec> hrec;
   void release() {
-    for (DevBuf* b : {&tab_mine, &tab_all, &tab_prev, &tchanged, &flags, &send[0], &send[1], &recv[0], &recv[1], &rec, &rec_all})
+    for (DevBuf* b : {&tab_mine, &tab_all, &tab_prev, &tchanged, &flags, &send[0], &send[1], &recv[0], &recv[1], &rec, &rec_all, &flab})
       b->release();
   }
 };
@@ -615,7 +616,13 @@ struct SlabEngine {
   SlabPlan pl;
   Geom gglob;
   Engine<T> eng;
-  uint32_t XY = 0, base = 0, own_lo = 0, own_hi = 0, act_lo = 0, act_hi = 0;
+  uint32_t XY = 0, own_lo = 0, own_hi = 0, act_lo = 0, act_hi = 0;
+  // global id of window vertex 0 (u64: a sharded field may exceed 2^32
+  // vertices) and the same for the EditSet; they differ only under the test
+  // bias MSSZ_SLAB_Z_BIAS, which places the field zbias planes deep inside a
+  // larger virtual grid so every internal global id exceeds 2^32
+  uint64_t base = 0, out_base = 0;
+  uint32_t zbias = 0;
   uint64_t n_glob = 0;
   SlabTable stab{};
   bool labels_verified = false;
@@ -624,19 +631,22 @@ struct SlabEngine {
              const mssz_cu_options& o)
       : tr(t), ws(w), sb(b), pl(p), gglob(gg), eng(w, gw, o) {
     XY = gg.XY;
-    base = pl.wz0 * XY;
+    if (const char* b = std::getenv("MSSZ_SLAB_Z_BIAS")) zbias = static_cast<uint32_t>(std::strtoul(b, nullptr, 10));
+    base = (uint64_t(pl.wz0) + zbias) * XY;
+    out_base = uint64_t(pl.wz0) * XY;
     own_lo = (pl.z0 - pl.wz0) * XY;
     own_hi = (pl.z1 - pl.wz0) * XY;
     act_lo = ((pl.z0 > 0 ? pl.z0 - 1 : 0) - pl.wz0) * XY;
     act_hi = (std::min(pl.Z, pl.z1 + 1) - pl.wz0) * XY;
-    n_glob = gg.n;
+    n_glob = uint64_t(gg.XY) * gg.Z;
     stab.P = pl.P;
     stab.XY = XY;
-    for (uint32_t r = 0; r <= pl.P; ++r) stab.z0[r] = static_cast<uint32_t>(uint64_t(pl.Z) * r / pl.P);
+    for (uint32_t r = 0; r <= pl.P; ++r) stab.z0[r] = static_cast<uint32_t>(uint64_t(pl.Z) * r / pl.P) + zbias;
     const size_t nw = eng.n();
-    sb.tab_mine.ensure(size_t(4) * XY * 4);
-    sb.tab_all.ensure(size_t(4) * XY * 4 * pl.P);
-    sb.tab_prev.ensure(size_t(4) * XY * 4 * pl.P);
+    sb.tab_mine.ensure(size_t(4) * XY * 8);
+    sb.tab_all.ensure(size_t(4) * XY * 8 * pl.P);
+    sb.tab_prev.ensure(size_t(4) * XY * 8 * pl.P);
+    sb.flab.ensure(size_t(2) * ((nw + 63) & ~size_t(63)) * 8);
     sb.tchanged.ensure(size_t(4) * XY * pl.P);
     for (int k = 0; k < 2; ++k) {
       sb.send[k].ensure(size_t(2) * XY * sizeof(BEdit<T>));
@@ -723,7 +733,8 @@ struct SlabEngine {
   // range), then the boundary tables.  finals: also write final global labels of
   // the active range to FM / Fm (f); g labels are resolved per tile by
   // k_rfix_tiles through SlabRes.
-  void labels(const uint8_t* dir, uint32_t* FM, uint32_t* Fm, bool finals, bool only_dirty = false) {
+  uint64_t* flab(int fam) const { return sb.flab.as<uint64_t>() + size_t(fam) * ((n() + 63) & ~uint32_t(63)); }
+  void labels(const uint8_t* dir, uint64_t* FM, uint64_t* Fm, bool finals, bool only_dirty = false) {
     uint32_t* M = eng.lab(2);
     uint32_t* m = eng.lab(3);
     // the tile store masks vertices outside [own_lo, own_hi) as extrema
@@ -732,18 +743,18 @@ struct SlabEngine {
     if (multi) {
       eng.pre(kProfLabelJump);
       k_publish_labels<<<blocks(4ull * XY), 256, 0, ws.stream>>>(M, m, eng.fin(0), eng.fin(1), XY, own_lo,
-                                                                  own_hi, base, sb.tab_mine.as<uint32_t>());
+                                                                  own_hi, base, sb.tab_mine.as<uint64_t>());
       eng.launched(kProfLabelJump);
-      tr.allgather_dev(sb.tab_mine.p, sb.tab_all.p, size_t(4) * XY * 4, ws.stream);
+      tr.allgather_dev(sb.tab_mine.p, sb.tab_all.p, size_t(4) * XY * 8, ws.stream);
       eng.pre(kProfLabelJump);
-      k_resolve_table<<<blocks(4ull * XY * pl.P, 16), 256, 0, ws.stream>>>(sb.tab_all.as<uint32_t>(), stab,
+      k_resolve_table<<<blocks(4ull * XY * pl.P, 16), 256, 0, ws.stream>>>(sb.tab_all.as<uint64_t>(), stab,
                                                                             sb.flags.as<uint32_t>());
       eng.launched(kProfLabelJump);
     }
     if (!finals) return;
     eng.pre(kProfLabelFinish);
     k_final_labels<<<blocks(act_hi - act_lo, 16), 256, 0, ws.stream>>>(
-        M, m, eng.fin(0), eng.fin(1), sb.tab_all.as<uint32_t>(), stab, act_lo, act_hi, base, multi ? 1 : 0,
+        M, m, eng.fin(0), eng.fin(1), sb.tab_all.as<uint64_t>(), stab, act_lo, act_hi, base, multi ? 1 : 0,
         FM, Fm);
     eng.launched(kProfLabelFinish);
   }
@@ -895,7 +906,7 @@ struct SlabEngine {
       const uint64_t tot = 4ull * XY * pl.P;
       if (incr) {
         eng.pre(kProfLabelJump);
-        k_table_diff<<<blocks(tot, 16), 256, 0, ws.stream>>>(sb.tab_all.as<uint32_t>(), sb.tab_prev.as<uint32_t>(),
+        k_table_diff<<<blocks(tot, 16), 256, 0, ws.stream>>>(sb.tab_all.as<uint64_t>(), sb.tab_prev.as<uint64_t>(),
                                                             sb.tchanged.as<uint8_t>(), tot,
                                                             sb.flags.as<uint32_t>() + 1);
         eng.launched(kProfLabelJump);
@@ -904,9 +915,9 @@ struct SlabEngine {
                                                             sb.flags.as<uint32_t>() + 1, stab, eng.geo, base);
         eng.launched(kProfLabelJump);
       } else {
-        CK(cudaMemcpyAsync(sb.tab_prev.p, sb.tab_all.p, tot * 4, cudaMemcpyDeviceToDevice, ws.stream));
+        CK(cudaMemcpyAsync(sb.tab_prev.p, sb.tab_all.p, tot * 8, cudaMemcpyDeviceToDevice, ws.stream));
       }
-      eng.sres = SlabRes{sb.tab_all.as<uint32_t>(), stab, base};
+      eng.sres = SlabRes{sb.tab_all.as<uint64_t>(), stab, base};
     } else {
       eng.sres = SlabRes{nullptr, stab, base};  // one slab: window labels are final
     }
@@ -995,7 +1006,9 @@ struct SlabEngine {
     eng.directions(d_f, ws.fdir.as<uint8_t>());
     eng.directions(S.g, S.gdir);
     CK(cudaEventRecord(ws.ev[1], ws.stream));
-    labels(S.fdir, eng.lab(0), eng.lab(1), true);
+    S.fM64 = flab(0);
+    S.fm64 = flab(1);
+    labels(S.fdir, flab(0), flab(1), true);
     gather();
     if (sum([](const Rec& r) { return r.err; }))
       fail(MSSZ_CU_ERR_INTERNAL, "path compression exceeded its round cap (corrupt direction field)");
@@ -1030,7 +1043,7 @@ struct SlabEngine {
   // this slab's part of edits() (edit_engine.cpp:368-378): global ids, sorted;
   // returns (local count, offset of this slab's part in the global EditSet, global count)
   void compact(uint64_t* d_idx, T* d_val, uint64_t& count, uint64_t& offset, uint64_t& total) {
-    count = eng.compact(s().touched, 1, s().g, d_idx, d_val, base);  // touched is 0 off the owned range
+    count = eng.compact(s().touched, 1, s().g, d_idx, d_val, out_base);  // touched is 0 off the owned range
     gather();  // ctl->mism holds the compaction count
     offset = 0;
     for (uint32_t r = 0; r < pl.r; ++r) offset += sb.hrec[r].mism;

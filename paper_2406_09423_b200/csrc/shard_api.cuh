@@ -6,6 +6,42 @@
 namespace mssz_b200 {
 namespace {
 
+// Global geometry of a z-slab sharded field: extents validated as
+// build_topology (grid.cpp:39-55, cap 2^40 vertices); the vertex count may
+// exceed 2^32 -- global ids are u64 in the sharded engine -- but a plane and
+// every rank's window must fit the device's u32 ids.  n is left 0 (the global
+// count is XY * Z in u64; only windows carry a device-sized n).
+Geom make_slab_geom(int ndims, const uint64_t* dims) {
+  if (ndims != 3) fail(MSSZ_CU_ERR_USAGE, "z-slab sharding needs a 3D grid");
+  if (!dims) fail(MSSZ_CU_ERR_USAGE, "dims is null");
+  const uint64_t cap = uint64_t(1) << 40;
+  uint64_t count = 1;
+  for (int a = 0; a < 3; ++a) {
+    if (dims[a] < 2) fail(MSSZ_CU_ERR_USAGE, "every grid extent must be >= 2");
+    if (dims[a] > cap / count) fail(MSSZ_CU_ERR_USAGE, "grid exceeds the address-space cap");
+    count *= dims[a];
+  }
+  if (dims[0] * dims[1] >= 0xFFFFFFFFull || dims[2] >= 0xFFFFFFFFull)
+    fail(MSSZ_CU_ERR_USAGE, "a z plane of %llu vertices exceeds the device's u32 ids",
+         (unsigned long long)(dims[0] * dims[1]));
+  Geom g{};
+  g.ndims = 3;
+  g.nst = 14;
+  g.X = static_cast<uint32_t>(dims[0]);
+  g.Y = static_cast<uint32_t>(dims[1]);
+  g.Z = static_cast<uint32_t>(dims[2]);
+  g.XY = g.X * g.Y;
+  g.n = 0;
+  for (int k = 0; k < 16; ++k) g.off[k] = 0;
+  for (int k = 0; k < g.nst; ++k) {
+    int dx, dy, dz;
+    stencil<3>(k, dx, dy, dz);
+    const int64_t o = dx + dy * static_cast<int64_t>(g.X) + dz * static_cast<int64_t>(g.XY);
+    g.off[k] = static_cast<int32_t>(static_cast<uint32_t>(static_cast<uint64_t>(o)));
+  }
+  return g;
+}
+
 Geom window_geom(const Geom& gg, const SlabPlan& pl) {
   const uint64_t d[3] = {gg.X, gg.Y, pl.wz1 - pl.wz0};
   return make_geom(3, d);
@@ -73,7 +109,7 @@ void slabs_local(int P, const int* devices, int ndevices, int ndims, const uint6
   if (ndims != 3) fail(MSSZ_CU_ERR_USAGE, "z-slab sharding needs a 3D grid");
   if (!f || !fh || !count_out || (capacity && (!idx || !val)))
     fail(MSSZ_CU_ERR_USAGE, "null input/output pointer");
-  const Geom gg = make_geom(ndims, dims);
+  const Geom gg = make_slab_geom(ndims, dims);
   const mssz_cu_options opt = resolve(o);
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -211,7 +247,7 @@ int mssz_cu_comm_destroy(mssz_cu_comm* c) {
       if (!c) fail(MSSZ_CU_ERR_USAGE, "null communicator");                                          \
       if (ndims != 3) fail(MSSZ_CU_ERR_USAGE, "z-slab sharding needs a 3D grid");                    \
       if (!f || !fh || !count || (cap && (!idx || !val))) fail(MSSZ_CU_ERR_USAGE, "null pointer");   \
-      const Geom gg = make_geom(ndims, dims);                                                        \
+      const Geom gg = make_slab_geom(ndims, dims);                                                   \
       mssz_cu_options opt = resolve(o);                                                              \
       opt.device = c->device;                                                                        \
       Workspace& ws = workspace(c->device);                                                          \
@@ -229,7 +265,7 @@ int mssz_cu_comm_destroy(mssz_cu_comm* c) {
       if (!c) fail(MSSZ_CU_ERR_USAGE, "null communicator");                                          \
       if (ndims != 3) fail(MSSZ_CU_ERR_USAGE, "z-slab sharding needs a 3D grid");                    \
       if (!f || !fh || !count || (cap && (!idx || !val))) fail(MSSZ_CU_ERR_USAGE, "null pointer");   \
-      const Geom gg = make_geom(ndims, dims);                                                        \
+      const Geom gg = make_slab_geom(ndims, dims);                                                   \
       mssz_cu_options opt = resolve(o);                                                              \
       opt.device = c->device;                                                                        \
       Workspace& ws = workspace(c->device);                                                          \

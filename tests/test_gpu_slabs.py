@@ -119,3 +119,32 @@ def test_slab_comm_single_rank(P):
     assert np.array_equal(got.indices, one.indices)
     assert got.values.tobytes() == one.values.tobytes()
     assert stats_dict(st) == stats_dict(st1)
+
+
+@pytest.mark.parametrize("kind,dims,seed,rel,dt,slabs", [
+    ("random-smooth", [40, 30, 20], 3, 1e-2, np.float32, (1, 2, 4)),
+    ("multi-scale", [48, 40, 32], 0, 1e-3, np.float32, (3, 8)),
+])
+def test_slabs_global_ids_beyond_u32(P, monkeypatch, kind, dims, seed, rel, dt, slabs):
+    """Global ids are u64 in the sharded engine (the reference caps grids at 2^40,
+    grid.cpp:19, not 2^32).  MSSZ_SLAB_Z_BIAS places the field that many planes
+    deep in a larger virtual grid, so every boundary edit, label-table entry and
+    resolved label carries a global id >= 2^32; any truncation to 32 bits would
+    break the table lookups and label comparisons."""
+    from paper_2406_09423_b200 import inputs as I
+    topo = P.build_topology(dims)
+    f = I.generate(kind, dims, seed, dt)
+    xi = I.resolve_rel(f, rel)
+    fh = I.compress_base(dims, f, xi)
+    opts = P.DeriveOptions(subloop_cap=100000)
+    st1 = P.EditStats()
+    one = P.derive_edits(topo, f, fh, xi, opts, st1)
+    xy = dims[0] * dims[1]
+    monkeypatch.setenv("MSSZ_SLAB_Z_BIAS", str((1 << 32) // xy + 7))
+    for p in slabs:
+        st = P.EditStats()
+        got = P.derive_edits_slabs(topo, f, fh, xi, p, opts, st)
+        assert np.array_equal(got.indices, one.indices), p
+        assert got.values.tobytes() == one.values.tobytes(), p
+        assert stats_dict(st) == stats_dict(st1), p
+
