@@ -225,7 +225,9 @@ int mssz_cu_classify_critical(uint64_t n, const uint64_t* asc, const uint64_t* d
  * its owned planes, as GLOBAL ids, sorted; concatenated in rank order they are
  * the EditSet of derive_edits (edit_engine.cpp:368-378) on the whole field, and
  * the result -- edits, values and EditStats -- is identical to the
- * single-device engine's.  Global vertex counts must be < 2^32 - 1.
+ * single-device engine's.  Global ids are u64: the whole field may hold up to
+ * the reference's 2^40 vertices (grid.cpp:19); a z plane and each rank's
+ * window must stay below 2^32 - 1 vertices (device-local ids are u32).
  *
  * One process per GPU: rank 0 calls mssz_cu_comm_unique_id and broadcasts the
  * id (e.g. torch.distributed), then every rank calls mssz_cu_comm_init

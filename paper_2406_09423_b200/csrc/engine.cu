@@ -163,7 +163,6 @@ struct Workspace {
   DevBuf f, g, fh, fdir, gdir, touched, stamp, fmark, lab, fin, lists, tiles;
   DevBuf tE, tEcnt, toldfin, tdirty, taffected, tbits, tcnt, tlist;  // label-tile store
   DevBuf xbuf;  // sparse R pass: crossing lists X (2 families x 2 buffers)
-  DevBuf cbits; // 1 bit per 64-vertex chunk whose direction codes changed
   DevBuf cstamp; // per 64-vertex chunk: mark of the last batch that changed a code (k_detect_dirty)
   Ctl* ctl = nullptr;
   Ctl* hctl = nullptr;  // pinned mirror
@@ -219,7 +218,7 @@ struct Workspace {
   }
   void release() {
     for (DevBuf* b : {&f, &g, &fh, &fdir, &gdir, &touched, &stamp, &fmark, &lab, &fin, &lists, &tiles,
-                      &tE, &tEcnt, &toldfin, &tdirty, &taffected, &tbits, &tcnt, &tlist, &xbuf, &cbits, &cstamp})
+                      &tE, &tEcnt, &toldfin, &tdirty, &taffected, &tbits, &tcnt, &tlist, &xbuf, &cstamp})
       b->release();
     next_batch = next_mark = 1;
   }
@@ -240,7 +239,6 @@ struct Workspace {
     // that may never have been exits before (their saved value only feeds the
     // change test of a tile that is dirty, hence recomputed, anyway)
     if (fin.ensure(np * 8)) CK(cudaMemsetAsync(fin.p, 0, fin.cap, stream));
-    cbits.ensure((n + 2047) / 2048 * 4 + 4);
     fresh |= cstamp.ensure((n + 63) / 64 * 4 + 4);
     lists.ensure(np * 16);  // list0 list1 S F (u32); reused as the u64+T EditSet
     tiles.ensure(((n + kCompactTile - 1) / kCompactTile + 1) * 4);
@@ -342,6 +340,7 @@ struct Engine {
   uint64_t r_last_mism = ~uint64_t(0);  // mismatches of the latest R iteration
   bool r_full_valid = false;            // tile label state matches gdir (no C edits since)
   bool x_valid = false;                 // crossing lists X match gdir (for k_cross_update)
+  uint32_t x_mark = 0;                  // first change mark issued after the current X
   int x_cur[2] = {0, 0};
   uint32_t x_n[2] = {0, 0};
   size_t prof_n = 0;
@@ -390,7 +389,6 @@ struct Engine {
     s.xi = 0;
     s.ctl = ws.ctl;
     s.tdirty = nullptr;
-    s.cdirty = ws.cbits.as<uint32_t>();
     s.cstamp = ws.cstamp.as<uint32_t>();
     s.own_lo = s.act_lo = 0;
     s.own_n = s.act_n = geo.n;
@@ -429,8 +427,7 @@ struct Engine {
 
   // K1 full sweep: 2.5D smem-tiled, chunk of the streamed axis sized for >= 8 CTAs/SM.
   void directions(const T* vals, uint8_t* dir) {
-    if (dir == s.gdir && s.cdirty)  // every code may change: X must re-evaluate all chunks
-      CK(cudaMemsetAsync(s.cdirty, 0xFF, (n() + 2047) / 2048 * 4, ws.stream));
+    if (dir == s.gdir) x_valid = false;  // every code may change: X is rebuilt from scratch
     if (dir == s.gdir) {
       for (bool& f : fresh) f = false;
       ++code_epoch;
@@ -911,14 +908,14 @@ struct Engine {
     uint32_t* upidx = fin(0);
     uint64_t* pv = reinterpret_cast<uint64_t*>(list(2));
     // 1. crossing lists X for both families: re-evaluate only 64-vertex chunks
-    //    whose codes changed since the last X (cdirty, set by every writer)
+    //    whose codes changed since the last X (change marks cstamp >= x_mark)
     const bool incremental = x_valid;
     uint32_t nxs[2];
     CK(cudaMemsetAsync(ws.ctl->sp_count, 0, 4 * sizeof(uint32_t), ws.stream));
     if (incremental) {
       pre(kProfSparse);
       k_cross_chunks<<<grid_for(uint64_t(x_n[0]) + x_n[1] + n() / 64, 256, ws.sms, 16), 256, 0,
-                       ws.stream>>>(s.gdir, s.fM, s.fm, geo, s.cdirty, xlist(0, x_cur[0]), x_n[0],
+                       ws.stream>>>(s.gdir, s.fM, s.fm, geo, s.cstamp, x_mark, xlist(0, x_cur[0]), x_n[0],
                                     xlist(1, x_cur[1]), x_n[1], xlist(0, x_cur[0] ^ 1),
                                     xlist(1, x_cur[1] ^ 1), ws.ctl->sp_count, x_cap());
       launched(kProfSparse);
@@ -937,7 +934,7 @@ struct Engine {
         launched(kProfSparse);
       }
     }
-    CK(cudaMemsetAsync(s.cdirty, 0, (n() + 2047) / 2048 * 4, ws.stream));
+    x_mark = ws.next_mark;  // changes after this X carry marks >= x_mark
     CK(cudaMemcpyAsync(nxs, ws.ctl->sp_count, sizeof nxs, cudaMemcpyDeviceToHost, ws.stream));
     ws.sync();
     x_valid = false;

@@ -698,7 +698,6 @@ struct State {
   double xi;
   Ctl* ctl;
   uint8_t* tdirty;  // R-loop only: label tiles whose direction codes changed
-  uint32_t* cdirty; // 1 bit per 64-vertex chunk whose codes changed (sparse R pass's X)
   // z-slab sharding (shard.cuh): fixes lower only targets in [own_lo, own_lo + own_n),
   // frontier refreshes only vertices in [act_lo, act_lo + act_n) (owned planes plus
   // one halo plane per side).  Single device: both ranges are the whole grid.
@@ -888,12 +887,11 @@ __device__ __forceinline__ void frontier_update(const State<T>& s, uint32_t ns, 
         // cu is u's pre-batch code: only the fmark winner writes gdir[u]
         if (cu != code) {
           s.gdir[u] = code;
+          // the chunk's change mark: incremental subloop detection
+          // (k_detect_dirty) and the sparse R pass's incremental X
+          // (k_cross_chunks) both read it
           if (s.cstamp && s.cstamp[u >> 6] != mark) s.cstamp[u >> 6] = mark;
           if (s.tdirty) s.tdirty[label_tile_of<DIM>(s.geo, ux, uy, uz)] = 1;
-          if (s.cdirty) {  // test first: neighbouring edits share the chunk bit
-            const uint32_t bit = 1u << ((u >> 6) & 31);
-            if (!(s.cdirty[u >> 11] & bit)) atomicOr(&s.cdirty[u >> 11], bit);
-          }
         }
       }
     }
@@ -2015,10 +2013,14 @@ __global__ void __launch_bounds__(256) k_cross(const uint8_t* __restrict__ gdir,
 
 // X maintained across any edits: both families at once.  Entries of the old
 // lists outside dirty chunks are kept; every vertex of a dirty chunk is
-// re-evaluated.  One warp per bitmap word; lanes cover a chunk's 64 vertices.
+// re-evaluated.  A chunk is dirty when a code in it changed since the old X:
+// its change mark (cstamp, written by every frontier refresh) is >= `since`,
+// the first mark issued after the old X (marks only grow; a full direction
+// sweep invalidates X instead).  One warp per 32 chunks; lanes cover a chunk's
+// 64 vertices.
 __global__ void __launch_bounds__(256) k_cross_chunks(
     const uint8_t* __restrict__ gdir, const uint32_t* __restrict__ fM,
-    const uint32_t* __restrict__ fm, Geom g, const uint32_t* __restrict__ cdirty,
+    const uint32_t* __restrict__ fm, Geom g, const uint32_t* __restrict__ cstamp, uint32_t since,
     const uint32_t* __restrict__ Xa_old, uint32_t na_old, const uint32_t* __restrict__ Xd_old,
     uint32_t nd_old, uint32_t* __restrict__ Xa, uint32_t* __restrict__ Xd, uint32_t* counts,
     uint32_t cap) {
@@ -2033,18 +2035,21 @@ __global__ void __launch_bounds__(256) k_cross_chunks(
     uint32_t v = 0;
     if (i < nold) {
       v = i < na_old ? Xa_old[i] : Xd_old[i - na_old];
-      const bool clean = !((__ldg(cdirty + (v >> 11)) >> ((v >> 6) & 31)) & 1u);
+      const bool clean = __ldg(cstamp + (v >> 6)) < since;
       ka = clean && i < na_old;
       kd = clean && i >= na_old;
     }
     warp_append_cap(ka, v, Xa, counts + 0, cap);
     warp_append_cap(kd, v, Xd, counts + 1, cap);
   }
-  // (b) re-evaluate dirty chunks
+  // (b) re-evaluate dirty chunks: a warp ballots the change marks of 32
+  // consecutive 64-vertex chunks
   const uint64_t nwords = (static_cast<uint64_t>(g.n) + 2047) / 2048;
+  const uint64_t nch = (static_cast<uint64_t>(g.n) + 63) / 64;
   const uint64_t wstride = stride / 32;
   for (uint64_t w = gtid / 32; w < nwords; w += wstride) {
-    uint32_t bits = __ldg(cdirty + w);
+    const uint64_t c = w * 32 + lane;
+    uint32_t bits = __ballot_sync(0xffffffffu, c < nch && __ldg(cstamp + c) >= since);
     while (bits) {
       const int b = __ffs(bits) - 1;
       bits &= bits - 1;

@@ -979,7 +979,6 @@ struct SlabEngine {
     eng.bind(d_f);
     State<T>& S = s();
     S.xi = xi;
-    S.cdirty = nullptr;
     S.own_lo = own_lo;
     S.own_n = own_hi - own_lo;
     S.act_lo = act_lo;
