@@ -675,7 +675,7 @@ struct Engine {
     else
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_subloop<T, 3>, kSubThreads, 0));
     if (occ < 1) fail(MSSZ_CU_ERR_CUDA, "persistent subloop kernel cannot be co-resident");
-    coop_blocks = ws.sms * std::min(occ, 2);
+    coop_blocks = ws.sms * std::min(occ, 3);
     return coop_blocks;
   }
 

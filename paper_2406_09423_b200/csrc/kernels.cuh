@@ -1231,7 +1231,11 @@ __device__ BatchResult small_batch(const State<T>& s, int kind, uint32_t n, uint
 }
 
 template <class T, int DIM>
-__global__ void __launch_bounds__(kSubThreads, 2)
+// 3 CTAs per SM (40 registers, a few spills): the kernel is bound by random
+// DRAM lines, and 75% occupancy keeps more of them in flight than 50% (C4:
+// 226.5 -> 208.1 ms per step); at 4 CTAs (32 registers) the spills dominate
+// (279.7 ms).
+__global__ void __launch_bounds__(kSubThreads, 3)
     k_subloop(State<T> s, int kind, uint64_t cap, uint32_t batch_base, uint32_t mark_base,
               uint32_t max_batches, uint32_t small_max, uint32_t huge_min, uint32_t park_cap) {
   cg::grid_group grid = cg::this_grid();
