@@ -709,6 +709,12 @@ struct State {
 // 0xF0000000, Workspace::ensure)
 constexpr uint32_t kParked = 0xFFFFFFFFu;
 
+// list items per lane per step in fix_batch (1 or 2; MSSZ_FIX_PER_LANE at build)
+#ifndef MSSZ_FIX_PER_LANE
+#define MSSZ_FIX_PER_LANE 2
+#endif
+constexpr int kFixPerLane = MSSZ_FIX_PER_LANE;
+
 // claim (edit_engine.cpp:160-169) + lower_step (:75-86): the first claimant of
 // t in this batch lowers it from the pre-batch value; exactly one winner per
 // target, so Σ winners == the reference's applied count.
@@ -732,38 +738,42 @@ __device__ __forceinline__ void fix_batch(const State<T>& s, const uint32_t* __r
                                           uint64_t tid, uint64_t stride, uint32_t* retry = nullptr,
                                           uint32_t* retry_count = nullptr, uint32_t* park = nullptr,
                                           uint32_t* park_count = nullptr) {
-  // two list items per lane per step: their loads and claims overlap
-  const uint64_t step = 2 * stride;
+  // J list items per lane per step: their loads and claims overlap
+  constexpr int J = kFixPerLane;
+  const uint64_t step = J * stride;
   __shared__ uint32_t sstage[kStageWarps][kStageK * 32], rstage[kStageWarps][kStageK * 32];
   WarpBuffer<kStageK> sbuf(warp_stage(sstage)), rbuf(warp_stage(rstage));
-  for (uint64_t wb = (tid & ~uint64_t(31)) * 2; wb < n; wb += step) {
-    const uint64_t i0 = wb + (threadIdx.x & 31), i1 = i0 + 32;
-    uint32_t t[2] = {0, 0};
-    bool live[2] = {i0 < n, i1 < n};
-    uint32_t v[2];
+  for (uint64_t wb = (tid & ~uint64_t(31)) * J; wb < n; wb += step) {
+    uint32_t t[J], v[J], prev[J];
+    bool live[J], ok[J];
 #pragma unroll
-    for (int j = 0; j < 2; ++j) v[j] = live[j] ? __ldcg(list + (j ? i1 : i0)) : 0u;
+    for (int j = 0; j < J; ++j) {
+      const uint64_t i = wb + (threadIdx.x & 31) + 32 * j;
+      live[j] = i < n;
+      v[j] = live[j] ? __ldcg(list + i) : 0u;
+      t[j] = 0;
+      prev[j] = batch;
+      ok[j] = false;
+    }
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < J; ++j) {
       if (!live[j]) continue;
       if (rule == 0) t[j] = v[j];
       else if (rule == 1) t[j] = v[j] + s.geo.off[__ldcg(s.gdir + v[j]) & 15u];
       else t[j] = v[j] + s.geo.off[__ldg(s.fdir + v[j]) >> 4];
     }
-    uint32_t prev[2] = {batch, batch};
 #pragma unroll
-    for (int j = 0; j < 2; ++j)  // only the owner of a target lowers it (owner-computes)
+    for (int j = 0; j < J; ++j)  // only the owner of a target lowers it (owner-computes)
       if (live[j] && t[j] - s.own_lo < s.own_n) prev[j] = atomicExch(&s.stamp[t[j]], batch);
-    T gv[2], fv[2];
+    T gv[J], fv[J];
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
+    for (int j = 0; j < J; ++j)
       if (prev[j] != batch) {
         gv[j] = __ldcg(s.g + t[j]);
         fv[j] = __ldg(s.f + t[j]);
       }
-    bool ok[2] = {false, false};
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < J; ++j) {
       T nv;
       if (prev[j] != batch && lower_value<T>(gv[j], fv[j], s.xi, nv)) {
         s.g[t[j]] = nv;
@@ -771,20 +781,18 @@ __device__ __forceinline__ void fix_batch(const State<T>& s, const uint32_t* __r
         ok[j] = true;
       }
     }
-    sbuf.push(ok[0], t[0], s.S, s_count);
-    sbuf.push(ok[1], t[1], s.S, s_count);
-    if (park) {  // won the claim, target at its floor: park the item (see k_subloop)
-      bool pk[2];
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        pk[j] = live[j] && prev[j] != batch && !ok[j];
-        if (pk[j]) s.fmark[v[j]] = kParked;
+    for (int j = 0; j < J; ++j) sbuf.push(ok[j], t[j], s.S, s_count);
+    if (park) {  // won the claim, target at its floor: park the item (see k_subloop)
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const bool pk = live[j] && prev[j] != batch && !ok[j];
+        if (pk) s.fmark[v[j]] = kParked;
+        rbuf.push(pk, v[j], park, park_count);
       }
-      rbuf.push(pk[0], v[0], park, park_count);
-      rbuf.push(pk[1], v[1], park, park_count);
     } else if (retry) {
-      rbuf.push(live[0] && !ok[0], v[0], retry, retry_count);
-      rbuf.push(live[1] && !ok[1], v[1], retry, retry_count);
+#pragma unroll
+      for (int j = 0; j < J; ++j) rbuf.push(live[j] && !ok[j], v[j], retry, retry_count);
     }
   }
   sbuf.flush(s.S, s_count);
@@ -1275,7 +1283,12 @@ __global__ void __launch_bounds__(kSubThreads, 3)
 
   uint32_t cur = *reinterpret_cast<volatile uint32_t*>(&ctl->cur);
   uint64_t attempted = *reinterpret_cast<volatile uint64_t*>(&ctl->attempted);
-  uint64_t iters = 0, edits = 0, frontier = 0, big = 0, small_ns = 0, big_ns = 0, items = 0;
+  // run statistics live in shared memory, kept by thread 0: as registers they
+  // stayed live across the inlined batch bodies and forced spills there
+  enum { kIters, kEdits, kFrontier, kBig, kItems, kSmallNs, kBigNs, kT0, kAcc };
+  __shared__ unsigned long long acc[kAcc];
+  if (threadIdx.x < kAcc) acc[threadIdx.x] = 0;
+  __syncthreads();
   uint32_t status = kStatusOk, done = 0, seq = 0;
   auto post = [&](uint32_t type, uint32_t n, uint32_t it) {
     if (threadIdx.x == 0) {
@@ -1316,8 +1329,11 @@ __global__ void __launch_bounds__(kSubThreads, 3)
     }
     const uint32_t it = static_cast<uint32_t>(attempted);
     BatchResult r;
-    uint64_t t0 = 0;
-    if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    if (threadIdx.x == 0) {
+      uint64_t t0;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      acc[kT0] = t0;
+    }
     bool fallback_only = false;
     for (;;) {  // at most twice: the rule pass, then (kNeedMerge) the fallback over list ∪ P
       if (n <= small_max) {
@@ -1325,7 +1341,7 @@ __global__ void __launch_bounds__(kSubThreads, 3)
       } else {
         post(fallback_only ? kCmdFallback : kCmdBatch, n, it);
         r = big_batch<T, DIM>(s, grid, kind, n, cur, it, batch_base, mark_base, fallback_only);
-        ++big;
+        if (threadIdx.x == 0) ++acc[kBig];
         __syncthreads();
       }
       if (r.applied != kNeedMerge) break;
@@ -1336,16 +1352,18 @@ __global__ void __launch_bounds__(kSubThreads, 3)
     if (threadIdx.x == 0) {
       uint64_t t1;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-      (n <= small_max ? small_ns : big_ns) += t1 - t0;
+      acc[n <= small_max ? kSmallNs : kBigNs] += t1 - acc[kT0];
     }
     if (r.applied == 0) {
       status = kStatusStall;
       break;
     }
-    ++iters;
-    edits += r.applied;
-    frontier += r.nf;
-    items += n;
+    if (threadIdx.x == 0) {
+      ++acc[kIters];
+      acc[kEdits] += r.applied;
+      acc[kFrontier] += r.nf;
+      acc[kItems] += n;
+    }
     cur ^= 1;
     ++done;
   }
@@ -1356,13 +1374,13 @@ __global__ void __launch_bounds__(kSubThreads, 3)
   if (threadIdx.x == 0) {
     ctl->cur = cur;
     ctl->attempted = attempted;
-    ctl->iters += iters;
-    ctl->edits += edits;
-    ctl->frontier += frontier;
-    ctl->big_batches += big;
-    ctl->items += items;
-    ctl->small_ns += small_ns;
-    ctl->big_ns += big_ns;
+    ctl->iters += acc[kIters];
+    ctl->edits += acc[kEdits];
+    ctl->frontier += acc[kFrontier];
+    ctl->big_batches += acc[kBig];
+    ctl->items += acc[kItems];
+    ctl->small_ns += acc[kSmallNs];
+    ctl->big_ns += acc[kBigNs];
     ctl->status = status;
   }
 }
