@@ -101,17 +101,25 @@ def kernel_parity(dims, f, g, R) -> dict:
 
 
 def c4(args) -> dict:
-    """C4 snapshots: full-field (1024^3) and middle z-sub-volume per-kernel parity."""
+    """Snapshots of a config's correction (default C4): full-field and (3D)
+    middle z-sub-volume per-kernel parity."""
     import gc
-    cfg = I.CONFIGS["C4"]
+    cfg = I.CONFIGS[args.config]
     dims = list(cfg.dims)
     t = time.perf_counter()
     f, fh, xi = I.make_inputs(cfg)
     gen_s = time.perf_counter() - t
-    X, Y, Z = dims
-    z0 = Z // 2 - args.planes // 2
-    sl = slice(z0 * X * Y, (z0 + args.planes) * X * Y)
-    sub_dims = [X, Y, args.planes]
+    if len(dims) == 3 and dims[2] > args.planes:
+        X, Y, Z = dims
+        z0 = Z // 2 - args.planes // 2
+        sl = slice(z0 * X * Y, (z0 + args.planes) * X * Y)
+        sub_dims = [X, Y, args.planes]
+    else:  # 2D or thin: no sub-volume
+        z0, sl, sub_dims = 0, None, None
+        if args.mode == "sub":
+            args.mode = "full"
+        elif args.mode == "both":
+            args.mode = "full"
     # kept states: after the first C pass; the state R iteration 1 starts from
     # (the last C pass before it); after R iterations 1, 10 and 20 of the run
     # (the start states of the next R batch when the R gate passes there); the
@@ -152,7 +160,7 @@ def c4(args) -> dict:
     res = {"workload": cfg.note, "dims": dims, "xi": xi, "input_gen_s": gen_s,
            "derive_with_snapshots_s": run_s, "edit_stats": {k: getattr(st, k) for k in STAT_KEYS},
            "reference_threads": THREADS, "full_field": [],
-           "sub_volume": {"dims": sub_dims, "z_planes": [z0, z0 + args.planes],
+           "sub_volume": {"dims": sub_dims, "z_planes": [z0, z0 + args.planes] if sub_dims else None,
                           "note": "the sub-volume is treated as its own grid (boundary planes clipped)",
                           "snapshots": []}}
     R = O.ref()
@@ -242,6 +250,7 @@ def derive_one(name) -> dict:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("what", choices=["c4", "derive"])
+    ap.add_argument("--config", default="C4", help="c4: which config's correction to snapshot")
     ap.add_argument("--mode", default="both", choices=["full", "sub", "both"])
     ap.add_argument("--out", default=None)
     ap.add_argument("--planes", type=int, default=128)
