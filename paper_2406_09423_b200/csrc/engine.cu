@@ -427,7 +427,9 @@ struct Engine {
 
   // K1 full sweep: 2.5D smem-tiled, chunk of the streamed axis sized for >= 8 CTAs/SM.
   void directions(const T* vals, uint8_t* dir) {
-    if (dir == s.gdir) x_valid = false;  // every code may change: X is rebuilt from scratch
+    // every code may change: every chunk counts as changed for the next
+    // incremental X (one pass over both families beats two full k_cross)
+    if (dir == s.gdir) x_mark = 0;
     if (dir == s.gdir) {
       for (bool& f : fresh) f = false;
       ++code_epoch;
@@ -606,7 +608,10 @@ struct Engine {
       fail(MSSZ_CU_ERR_INTERNAL, "path compression exceeded its round cap (corrupt direction field)");
     if (finish) {
       pre(kProfLabelFinish);
-      k_label_finish<<<grid_for(n() / 4 + 1, 256, ws.sms, 16), 256, 0, ws.stream>>>(M, m, fM, fm, n());
+      if (geo.ndims == 2)
+        k_label_finish_tiles<2><<<ts.ntiles, 256, 0, ws.stream>>>(M, m, fM, fm, geo);
+      else
+        k_label_finish_tiles<3><<<ts.ntiles, 256, 0, ws.stream>>>(M, m, fM, fm, geo);
       launched(kProfLabelFinish);
     }
     CK(cudaEventRecord(ws.ev[3], ws.stream));

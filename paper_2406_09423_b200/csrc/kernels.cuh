@@ -1817,23 +1817,49 @@ __global__ void __launch_bounds__(256) k_label_exit_jump(uint32_t* __restrict__ 
 }
 
 // Phase 3 (f labels only): final label of every vertex, lab[v] = fin[lab[v]].
-__global__ void __launch_bounds__(256) k_label_finish(uint32_t* __restrict__ M,
-                                                      uint32_t* __restrict__ m,
-                                                      const uint32_t* __restrict__ finM,
-                                                      const uint32_t* __restrict__ finm, uint32_t n) {
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  const uint64_t n4 = n / 4;
-  for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n4;
-       q += stride) {
-    const uint4 a = reinterpret_cast<const uint4*>(M)[q];
-    const uint4 d = reinterpret_cast<const uint4*>(m)[q];
-    reinterpret_cast<uint4*>(M)[q] = make_uint4(finM[a.x], finM[a.y], finM[a.z], finM[a.w]);
-    reinterpret_cast<uint4*>(m)[q] = make_uint4(finm[d.x], finm[d.y], finm[d.z], finm[d.w]);
-  }
-  for (uint64_t v = n4 * 4 + static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < n;
-       v += stride) {
-    M[v] = finM[M[v]];
-    m[v] = finm[m[v]];
+// Phase 3, tile-ordered: one CTA per label tile, so the fin[] gathers of its
+// vertices (their chain roots inside the tile, or exits next to it) stay in
+// the tile's neighbourhood while it is resident in L2, instead of spreading
+// over the 16 planes a tile spans when the field is walked in index order.
+template <int DIM>
+__global__ void __launch_bounds__(256) k_label_finish_tiles(uint32_t* __restrict__ M, uint32_t* __restrict__ m,
+                                                            const uint32_t* __restrict__ finM,
+                                                            const uint32_t* __restrict__ finm, Geom g) {
+  using TL = LabelTile<DIM>;
+  const uint32_t ntx = (g.X + TL::TX - 1) / TL::TX;
+  const uint32_t nty = (g.Y + TL::TY - 1) / TL::TY;
+  const uint32_t b = blockIdx.x;
+  const uint32_t tx = b % ntx, ty = (b / ntx) % nty, tz = b / (ntx * nty);
+  const uint32_t x0 = tx * TL::TX, y0 = ty * TL::TY, z0 = tz * TL::TZ;
+  const int ex = min(TL::TX, static_cast<int>(g.X - x0));
+  const int ey = min(TL::TY, static_cast<int>(g.Y - y0));
+  const int ez = DIM == 2 ? 1 : min(TL::TZ, static_cast<int>(g.Z - z0));
+  const uint32_t base = x0 + g.X * y0 + g.XY * z0;
+  // four vertices per thread per step: their gathers overlap
+  for (int i0 = threadIdx.x; i0 < kLabelTileN; i0 += 4 * blockDim.x) {
+    uint32_t v[4], a[4], d[4];
+    bool in[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = i0 + q * blockDim.x;
+      const int lx = i & (TL::TX - 1), ly = (i >> TL::LX) & (TL::TY - 1), lz = i >> (TL::LX + TL::LY);
+      in[q] = lx < ex && ly < ey && lz < ez;
+      v[q] = base + lx + g.X * ly + g.XY * lz;
+      a[q] = in[q] ? M[v[q]] : 0u;
+      d[q] = in[q] ? m[v[q]] : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (!in[q]) continue;
+      a[q] = __ldg(finM + a[q]);
+      d[q] = __ldg(finm + d[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (in[q]) {
+        M[v[q]] = a[q];
+        m[v[q]] = d[q];
+      }
   }
 }
 
@@ -2037,9 +2063,9 @@ __global__ void __launch_bounds__(256) k_cross(const uint8_t* __restrict__ gdir,
 // lists outside dirty chunks are kept; every vertex of a dirty chunk is
 // re-evaluated.  A chunk is dirty when a code in it changed since the old X:
 // its change mark (cstamp, written by every frontier refresh) is >= `since`,
-// the first mark issued after the old X (marks only grow; a full direction
-// sweep invalidates X instead).  One warp per 32 chunks; lanes cover a chunk's
-// 64 vertices.
+// the first mark issued after the old X (marks only grow; after a full
+// direction sweep `since` is 0: every chunk is re-evaluated).  One warp per 32
+// chunks; lanes cover a chunk's 64 vertices.
 __global__ void __launch_bounds__(256) k_cross_chunks(
     const uint8_t* __restrict__ gdir, const uint32_t* __restrict__ fM,
     const uint32_t* __restrict__ fm, Geom g, const uint32_t* __restrict__ cstamp, uint32_t since,
