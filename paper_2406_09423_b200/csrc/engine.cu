@@ -298,7 +298,7 @@ uint32_t kSmallBatchMax = 256;  // tunable via MSSZ_SMALL_MAX (experiments)
 // worklists above n / kHugeBatchDivisor are run by host-launched streaming kernels
 uint32_t kHugeBatchDivisor = 64;  // tunable via MSSZ_HUGE_DIVISOR (experiments)
 // R batches applying more than n / kRHugeDivisor edits refresh with a full sweep
-uint32_t kRHugeDivisor = 512;     // tunable via MSSZ_RHUGE_DIVISOR
+uint32_t kRHugeDivisor = 256;     // tunable via MSSZ_RHUGE_DIVISOR (round-2 sweep: 128-256 best)
 // R iterations after one with fewer than n / kSparseMismDivisor mismatches use the
 // sparse pass; it gives up when Up(X) exceeds n / kSparseUpDivisor vertices
 uint32_t kSparseMismDivisor = 64;
