@@ -917,27 +917,18 @@ struct Engine {
     const bool incremental = x_valid;
     uint32_t nxs[2];
     CK(cudaMemsetAsync(ws.ctl->sp_count, 0, 4 * sizeof(uint32_t), ws.stream));
-    if (incremental) {
+    {
+      // from scratch (no X yet): every chunk is changed (since = 0) and there
+      // are no old entries -- one pass for both families (round 2: -1.3 ms per
+      // C4 step against one k_cross per family)
+      const uint32_t since = incremental ? x_mark : 0u;
+      const uint32_t na = incremental ? x_n[0] : 0u, nd = incremental ? x_n[1] : 0u;
       pre(kProfSparse);
-      k_cross_chunks<<<grid_for(uint64_t(x_n[0]) + x_n[1] + n() / 64, 256, ws.sms, 16), 256, 0,
-                       ws.stream>>>(s.gdir, s.fM, s.fm, geo, s.cstamp, x_mark, xlist(0, x_cur[0]), x_n[0],
-                                    xlist(1, x_cur[1]), x_n[1], xlist(0, x_cur[0] ^ 1),
+      k_cross_chunks<<<grid_for(uint64_t(na) + nd + n() / 64, 256, ws.sms, 16), 256, 0,
+                       ws.stream>>>(s.gdir, s.fM, s.fm, geo, s.cstamp, since, xlist(0, x_cur[0]), na,
+                                    xlist(1, x_cur[1]), nd, xlist(0, x_cur[0] ^ 1),
                                     xlist(1, x_cur[1] ^ 1), ws.ctl->sp_count, x_cap());
       launched(kProfSparse);
-    } else {
-      for (int fam = 0; fam < 2; ++fam) {
-        const uint32_t* fL = fam ? s.fm : s.fM;
-        uint32_t* out = xlist(fam, x_cur[fam] ^ 1);
-        uint32_t* cnt = &ws.ctl->sp_count[fam];
-        pre(kProfSparse);
-        if (geo.ndims == 2)
-          k_cross<2><<<grid_for(n(), 256, ws.sms, 16), 256, 0, ws.stream>>>(s.gdir, fL, geo, fam,
-                                                                           out, cnt, x_cap());
-        else
-          k_cross<3><<<grid_for(n(), 256, ws.sms, 16), 256, 0, ws.stream>>>(s.gdir, fL, geo, fam,
-                                                                           out, cnt, x_cap());
-        launched(kProfSparse);
-      }
     }
     x_mark = ws.next_mark;  // changes after this X carry marks >= x_mark
     CK(cudaMemcpyAsync(nxs, ws.ctl->sp_count, sizeof nxs, cudaMemcpyDeviceToHost, ws.stream));

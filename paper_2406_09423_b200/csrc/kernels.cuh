@@ -2041,27 +2041,9 @@ __global__ void __launch_bounds__(256) k_expand_targets(State<T> s, const uint32
 //   leaving Up(X) ends with the f label of its first outside vertex), and
 //   emit the batch targets of divergent mismatched vertices -- the same target
 //   set as the full pass.
-template <int DIM>
-__global__ void __launch_bounds__(256) k_cross(const uint8_t* __restrict__ gdir,
-                                               const uint32_t* __restrict__ fL, Geom g, int fam,
-                                               uint32_t* __restrict__ X, uint32_t* count,
-                                               uint32_t cap) {
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t wb = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) & ~uint64_t(31);
-       wb < g.n; wb += stride) {
-    const uint64_t v = wb + (threadIdx.x & 31);
-    bool cross = false;
-    if (v < g.n) {
-      const uint32_t c = (__ldg(gdir + v) >> (4 * fam)) & 15u;
-      if (c != kSelf) cross = __ldg(fL + v + g.off[c]) != __ldg(fL + v);
-    }
-    warp_append_cap(cross, static_cast<uint32_t>(v), X, count, cap);
-  }
-}
-
-// X maintained across any edits: both families at once.  Entries of the old
-// lists outside dirty chunks are kept; every vertex of a dirty chunk is
-// re-evaluated.  A chunk is dirty when a code in it changed since the old X:
+// X built (from scratch: since = 0, no old lists) or maintained across any
+// edits, both families at once.  Entries of the old lists outside dirty chunks
+// are kept; every vertex of a dirty chunk is re-evaluated.  A chunk is dirty when a code in it changed since the old X:
 // its change mark (cstamp, written by every frontier refresh) is >= `since`,
 // the first mark issued after the old X (marks only grow; after a full
 // direction sweep `since` is 0: every chunk is re-evaluated).  One warp per 32
