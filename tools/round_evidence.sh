@@ -1,4 +1,4 @@
-# round-2 final evidence v2 (HEAD)
+# round-2 evidence recipe (HEAD): GPU tests, smoke, bench lines + reference arm, launch list, DRAM traffic, sanitizers, C4 snapshot parity
 mkdir -p gpurun_out
 timeout -s ABRT 1200 python -m pytest tests -q -m gpu -o faulthandler_timeout=300 > gpurun_out/f2_pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/f2_pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/f2_smoke.log 2>&1; tail -1 gpurun_out/f2_smoke.log
