@@ -337,6 +337,7 @@ struct Engine {
   int coop_blocks = 0;
   std::vector<T> host_g;  // on_batch snapshots only
   bool trace = std::getenv("MSSZ_TRACE") != nullptr;  // per-iteration log on stderr
+  bool k1_reg3 = std::getenv("MSSZ_K1_REG3") != nullptr;  // A/B: the shared-memory K1 (k_directions_reg3)
   uint64_t r_last_mism = ~uint64_t(0);  // mismatches of the latest R iteration
   bool r_full_valid = false;            // tile label state matches gdir (no C edits since)
   bool x_valid = false;                 // crossing lists X match gdir (for k_cross_update)
@@ -443,6 +444,17 @@ struct Engine {
       chunk = std::min<uint32_t>(chunk, 64);
       dim3 grid(bx, (geo.Y + chunk - 1) / chunk);
       k_directions_tiled<T, 2><<<grid, DT::BX * DT::BY, 0, ws.stream>>>(vals, dir, geo, chunk);
+    } else if (sizeof(T) == 4 && !k1_reg3) {
+      // register-column K1: >= ~4 waves of 2 CTAs/SM, chunks of >= 8 planes
+      const uint32_t bx = (geo.X + kK1Cols - 1) / kK1Cols;
+      const uint32_t by = (geo.Y + kK1Warps * kK1R - 1) / (kK1Warps * kK1R);
+      const uint64_t tiles = uint64_t(bx) * by;
+      const uint32_t zc = static_cast<uint32_t>(std::min<uint64_t>(
+          std::max<uint64_t>(1, (uint64_t(ws.sms) * 8 + tiles - 1) / tiles), std::max<uint32_t>(1, geo.Z / 8)));
+      const uint32_t chunk = (geo.Z + zc - 1) / zc;
+      dim3 grid(bx, by, (geo.Z + chunk - 1) / chunk);
+      k_directions_col3<<<grid, kK1Warps * 32, 0, ws.stream>>>(reinterpret_cast<const float*>(vals), dir, geo,
+                                                              static_cast<int>(chunk));
     } else if (sizeof(T) == 4) {
       const uint32_t bx = (geo.X + kD3W - 1) / kD3W, by = (geo.Y + kD3H - 1) / kD3H;
       const uint64_t tiles = uint64_t(bx) * by;

@@ -621,6 +621,155 @@ __global__ void __launch_bounds__(kD3Warps * 32, kMinBlocks)
   }
 }
 
+// K1 (3D, f32, register columns) -- the default 3D f32 sweep since round 2.
+// Same cube decomposition as the block forms above, rearranged so that no
+// shared memory, no barrier and no packed position fields are involved:
+//  * the up-cube of (x,y,z) is {x,x+1} x {y,y+1} x {z,z+1}; the link of a
+//    vertex plus itself is up-cube(x,y,z) (VA) ∪ up-cube(x-1,y-1,z-1) (C),
+//    with index ranges C <= self <= VA;
+//  * a lane owns one column x (lanes 0..31 cover x0-1 .. x0+30; lanes 1..30
+//    produce output) and a warp kK1R consecutive output rows, streaming z;
+//  * every extreme is built separably: x-pairs (x, x+1) via one shuffle, cells
+//    by joining the x-pairs of rows y and y+1 (registers of the same lane),
+//    cubes by joining the cells of planes z and z+1 (the previous plane's
+//    cells stay in registers), C by shuffling the previous plane's cube of row
+//    y-1 up one lane;
+//  * a level joins (lower, upper) halves whose indices are all ordered lower <
+//    upper, so the SoS tie-break is ">= keeps upper" ascending and "< takes
+//    upper" descending at every level, exactly the scan order of sos_greater /
+//    sos_less (grid.hpp:53-63) over index-ranked slots;
+//  * positions are cube corner ids pre-multiplied by 4 (x: 4, y: 8, z: 16), so
+//    the final slot is one shift of a 32-bit half of kBlockSlot3.
+// Out-of-grid vertices hold key 0 (key-1 = ~0 descending): they never win.
+constexpr int kK1R = 8;      // output rows per warp
+constexpr int kK1Warps = 8;  // warps per CTA, stacked in y
+constexpr int kK1Cols = 30;  // output columns per warp (lanes 1..30)
+
+struct K1Ext {
+  uint32_t ak, ap;  // ascending: key, position * 4
+  uint32_t dk, dp;  // descending: key - 1, position * 4
+};
+
+// join(lower, upper): `bit` is the upper half's position bit (pre-multiplied)
+__device__ __forceinline__ K1Ext k1_join(const K1Ext& lo, const K1Ext& hi, uint32_t bit) {
+  K1Ext r;
+  const bool ta = hi.ak >= lo.ak;
+  r.ak = ta ? hi.ak : lo.ak;
+  r.ap = ta ? (hi.ap | bit) : lo.ap;
+  const bool td = hi.dk < lo.dk;
+  r.dk = td ? hi.dk : lo.dk;
+  r.dp = td ? (hi.dp | bit) : lo.dp;
+  return r;
+}
+
+__device__ __forceinline__ K1Ext k1_xpair(uint32_t k) {  // (x, x+1) of one row
+  const uint32_t k1 = __shfl_down_sync(0xffffffffu, k, 1);
+  K1Ext r;
+  const bool ta = k1 >= k;
+  r.ak = ta ? k1 : k;
+  r.ap = ta ? 4u : 0u;
+  const bool td = k1 - 1 < k - 1;
+  r.dk = td ? k1 - 1 : k - 1;
+  r.dp = td ? 4u : 0u;
+  return r;
+}
+
+__device__ __forceinline__ uint32_t k1_code(const K1Ext& va, const K1Ext& c) {
+  constexpr uint32_t kLoC = static_cast<uint32_t>(kBlockSlot3);         // C cube corners
+  constexpr uint32_t kHiVA = static_cast<uint32_t>(kBlockSlot3 >> 32);  // VA cube corners
+  const bool ta = va.ak >= c.ak;
+  const uint32_t sa = (ta ? kHiVA : kLoC) >> (ta ? va.ap : c.ap);
+  const bool td = va.dk < c.dk;
+  const uint32_t sd = (td ? kHiVA : kLoC) >> (td ? va.dp : c.dp);
+  return (sa & 15u) | ((sd & 15u) << 4);
+}
+
+// one plane step: keys of plane q (k) -> cells(q), cubes(q-1) from cells(q-1)
+// (kept per thread in shared memory, `cell`) and cells(q), codes of plane q-1
+// when `emit`, then C <- cubes(q-1) of rows y-1 one lane to the left
+__device__ __forceinline__ void k1_plane(const uint32_t (&k)[kK1R + 2], uint4* cell, K1Ext (&C)[kK1R],
+                                         bool cubes, bool emit, uint8_t* out, uint32_t X, uint32_t rows_out) {
+  K1Ext xp = k1_xpair(k[0]);
+  K1Ext held;  // cube of row j-1 shifted up one lane, parked until row j-1's codes are out
+#pragma unroll
+  for (int j = 0; j <= kK1R; ++j) {
+    const K1Ext xq = k1_xpair(k[j + 1]);
+    const K1Ext nw = k1_join(xp, xq, 8u);
+    xp = xq;
+    uint4& slot = cell[j * kK1Warps * 32];
+    if (cubes) {
+      const uint4 p = slot;
+      const K1Ext cube = k1_join(K1Ext{p.x, p.y, p.z, p.w}, nw, 16u);
+      if (j >= 1) {
+        // output row j-1: VA = cube row j, C = previous plane's cube row j-1 (lane - 1)
+        const uint32_t code = k1_code(cube, C[j - 1]);
+        if (emit && static_cast<uint32_t>(j - 1) < rows_out) out[static_cast<uint64_t>(j - 1) * X] = static_cast<uint8_t>(code);
+        C[j - 1] = held;
+      }
+      if (j < kK1R) {
+        held.ak = __shfl_up_sync(0xffffffffu, cube.ak, 1);
+        held.ap = __shfl_up_sync(0xffffffffu, cube.ap, 1);
+        held.dk = __shfl_up_sync(0xffffffffu, cube.dk, 1);
+        held.dp = __shfl_up_sync(0xffffffffu, cube.dp, 1);
+      }
+    }
+    slot = make_uint4(nw.ak, nw.ap, nw.dk, nw.dp);
+  }
+}
+
+__global__ void __launch_bounds__(kK1Warps * 32, 2)
+    k_directions_col3(const float* __restrict__ vals, uint8_t* __restrict__ dir, Geom g, int chunk) {
+  constexpr int R = kK1R;
+  // previous plane's cells, [row][thread] (conflict-free 16-byte slots)
+  __shared__ uint4 scell[(R + 1) * kK1Warps * 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int x = static_cast<int>(blockIdx.x) * kK1Cols - 1 + lane;
+  const int y0 = (static_cast<int>(blockIdx.y) * kK1Warps + w) * R;  // first output row
+  const int X = static_cast<int>(g.X), Y = static_cast<int>(g.Y), Z = static_cast<int>(g.Z);
+  const int s0 = static_cast<int>(blockIdx.z) * chunk, s1 = min(s0 + chunk, Z);
+  if (y0 >= Y) return;  // warp-uniform; no block-wide barrier below
+  const bool xok = x >= 0 && x < X;
+  uint32_t rowok = 0;  // key rows y0-1 .. y0+R
+#pragma unroll
+  for (int r = 0; r < R + 2; ++r) rowok |= (y0 - 1 + r >= 0 && y0 - 1 + r < Y ? 1u : 0u) << r;
+  if (!xok) rowok = 0;
+  const bool out_lane = lane >= 1 && lane <= kK1Cols && xok;
+  const uint32_t rows_out = out_lane ? static_cast<uint32_t>(min(R, Y - y0)) : 0u;
+  uint4* cell = scell + threadIdx.x;
+  // row r of plane q sits at q*XY + (y0-1+r)*X + x (u32: N < 2^32 per device)
+  const uint32_t base = static_cast<uint32_t>(y0 - 1) * g.X + static_cast<uint32_t>(x);
+  const uint32_t X1 = g.X;
+  auto load = [&](int q, float (&v)[R + 2]) {
+    const uint32_t ok = (q >= 0 && q < Z) ? rowok : 0u;
+    const uint32_t pb = base + static_cast<uint32_t>(q) * g.XY;  // wraps for row y0-1 = -1
+#pragma unroll
+    for (int r = 0; r < R + 2; ++r) v[r] = ((ok >> r) & 1u) ? __ldg(vals + (pb + r * X1)) : 0.f;
+  };
+  auto keys = [&](int q, const float (&v)[R + 2], uint32_t (&k)[R + 2]) {
+    const uint32_t ok = (q >= 0 && q < Z) ? rowok : 0u;
+#pragma unroll
+    for (int r = 0; r < R + 2; ++r) k[r] = ((ok >> r) & 1u) ? fkey(v[r]) : 0u;
+  };
+  float v[R + 2];
+  uint32_t k[R + 2];
+  K1Ext C[R];
+  load(s0 - 1, v);
+  // q = s0-1: cells only; q = s0: cubes(s0-1) -> C; then one plane per trip
+  keys(s0 - 1, v, k);
+  load(s0, v);
+  k1_plane(k, cell, C, false, false, nullptr, g.X, 0);
+  keys(s0, v, k);
+  load(s0 + 1, v);
+  k1_plane(k, cell, C, true, false, nullptr, g.X, 0);
+  uint8_t* out = dir + (base + g.X) + static_cast<uint64_t>(s0) * g.XY;  // row y0, plane s0
+  for (int q = s0 + 1; q <= s1; ++q) {
+    keys(q, v, k);
+    load(q + 1, v);
+    k1_plane(k, cell, C, true, true, out, g.X, rows_out);
+    out += g.XY;
+  }
+}
+
 // K1b (k_detect_kind, the full detect sweep) is defined with the subloop helpers below.
 
 // Counts of the first-match classes (detect_false_critical, edit_engine.cpp:134-158)
