@@ -196,6 +196,8 @@ struct Workspace {
                             static_cast<int>(label_tile_smem<2>())));
     CK(cudaFuncSetAttribute(k_label_tile<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(label_tile_smem<3>())));
+    CK(cudaFuncSetAttribute(k_directions_col3, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(k1_smem_bytes())));
     CK(cudaFuncSetAttribute(k_directions_reg3<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(sizeof(D3Smem))));
     CK(cudaFuncSetAttribute(k_directions_reg3<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -453,7 +455,7 @@ struct Engine {
           std::max<uint64_t>(1, (uint64_t(ws.sms) * 8 + tiles - 1) / tiles), std::max<uint32_t>(1, geo.Z / 8)));
       const uint32_t chunk = (geo.Z + zc - 1) / zc;
       dim3 grid(bx, by, (geo.Z + chunk - 1) / chunk);
-      k_directions_col3<<<grid, kK1Warps * 32, 0, ws.stream>>>(reinterpret_cast<const float*>(vals), dir, geo,
+      k_directions_col3<<<grid, kK1Warps * 32, k1_smem_bytes(), ws.stream>>>(reinterpret_cast<const float*>(vals), dir, geo,
                                                               static_cast<int>(chunk));
     } else if (sizeof(T) == 4) {
       const uint32_t bx = (geo.X + kD3W - 1) / kD3W, by = (geo.Y + kD3H - 1) / kD3H;

@@ -662,14 +662,15 @@ __device__ __forceinline__ K1Ext k1_join(const K1Ext& lo, const K1Ext& hi, uint3
   return r;
 }
 
-__device__ __forceinline__ K1Ext k1_xpair(uint32_t k) {  // (x, x+1) of one row
+__device__ __forceinline__ K1Ext k1_xpair(uint32_t k, uint32_t dk) {  // (x, x+1) of one row
   const uint32_t k1 = __shfl_down_sync(0xffffffffu, k, 1);
+  const uint32_t dk1 = __shfl_down_sync(0xffffffffu, dk, 1);
   K1Ext r;
   const bool ta = k1 >= k;
   r.ak = ta ? k1 : k;
   r.ap = ta ? 4u : 0u;
-  const bool td = k1 - 1 < k - 1;
-  r.dk = td ? k1 - 1 : k - 1;
+  const bool td = dk1 < dk;
+  r.dk = td ? dk1 : dk;
   r.dp = td ? 4u : 0u;
   return r;
 }
@@ -684,24 +685,27 @@ __device__ __forceinline__ uint32_t k1_code(const K1Ext& va, const K1Ext& c) {
   return (sa & 15u) | ((sd & 15u) << 4);
 }
 
-// one plane step: keys of plane q (k) -> cells(q), cubes(q-1) from cells(q-1)
-// (kept per thread in shared memory, `cell`) and cells(q), codes of plane q-1
-// when `emit`, then C <- cubes(q-1) of rows y-1 one lane to the left
-__device__ __forceinline__ void k1_plane(const uint32_t (&k)[kK1R + 2], uint4* cell, K1Ext (&C)[kK1R],
-                                         bool cubes, bool emit, uint8_t* out, uint32_t X, uint32_t rows_out) {
-  K1Ext xp = k1_xpair(k[0]);
-  K1Ext held;  // cube of row j-1 shifted up one lane, parked until row j-1's codes are out
+// one plane step: keys of plane q (k, dk = k - 1) -> cells(q), cubes(q-1) from
+// cells(q-1) (per thread and row in shared memory, `cell`) and cells(q), codes
+// of plane q-1 when `emit`, then C <- cubes(q-1) of rows y-1 one lane to the left
+// (shuffled: no shared-memory traffic)
+__device__ __forceinline__ void k1_plane(const uint32_t (&k)[kK1R + 2], const uint32_t (&dk)[kK1R + 2],
+                                         uint4* cell, K1Ext (&C)[kK1R], bool cubes, bool emit, uint8_t* out,
+                                         uint32_t X, uint32_t rows_out) {
+  constexpr int kStride = kK1Warps * 32;
+  K1Ext xp = k1_xpair(k[0], dk[0]);
+  K1Ext held;  // this plane's cube of row j-1 shifted up one lane, parked until row j-1's codes are out
 #pragma unroll
   for (int j = 0; j <= kK1R; ++j) {
-    const K1Ext xq = k1_xpair(k[j + 1]);
+    const K1Ext xq = k1_xpair(k[j + 1], dk[j + 1]);
     const K1Ext nw = k1_join(xp, xq, 8u);
     xp = xq;
-    uint4& slot = cell[j * kK1Warps * 32];
+    uint4& slot = cell[j * kStride];
     if (cubes) {
       const uint4 p = slot;
       const K1Ext cube = k1_join(K1Ext{p.x, p.y, p.z, p.w}, nw, 16u);
       if (j >= 1) {
-        // output row j-1: VA = cube row j, C = previous plane's cube row j-1 (lane - 1)
+        // output row j-1: VA = cube row j, C = previous plane's cube row j-1 of lane - 1
         const uint32_t code = k1_code(cube, C[j - 1]);
         if (emit && static_cast<uint32_t>(j - 1) < rows_out) out[static_cast<uint64_t>(j - 1) * X] = static_cast<uint8_t>(code);
         C[j - 1] = held;
@@ -717,11 +721,14 @@ __device__ __forceinline__ void k1_plane(const uint32_t (&k)[kK1R + 2], uint4* c
   }
 }
 
+constexpr size_t k1_smem_bytes() { return sizeof(uint4) * (kK1R + 1) * kK1Warps * 32; }
+
 __global__ void __launch_bounds__(kK1Warps * 32, 2)
     k_directions_col3(const float* __restrict__ vals, uint8_t* __restrict__ dir, Geom g, int chunk) {
   constexpr int R = kK1R;
-  // previous plane's cells, [row][thread] (conflict-free 16-byte slots)
-  __shared__ uint4 scell[(R + 1) * kK1Warps * 32];
+  // per [row][thread] 16-byte slots (conflict-free): the previous plane's cells (rows 0..R)
+  extern __shared__ uint4 k1_smem[];  // k1_smem_bytes()
+  uint4* scell = k1_smem;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int x = static_cast<int>(blockIdx.x) * kK1Cols - 1 + lane;
   const int y0 = (static_cast<int>(blockIdx.y) * kK1Warps + w) * R;  // first output row
@@ -739,33 +746,49 @@ __global__ void __launch_bounds__(kK1Warps * 32, 2)
   // row r of plane q sits at q*XY + (y0-1+r)*X + x (u32: N < 2^32 per device)
   const uint32_t base = static_cast<uint32_t>(y0 - 1) * g.X + static_cast<uint32_t>(x);
   const uint32_t X1 = g.X;
+  // out-of-grid rows load vertex 0 (their keys are forced to 0): no predicated
+  // loads; warps whose rows and columns are all inside skip the per-row tests
+  constexpr uint32_t kAll = (1u << (R + 2)) - 1;
+  const bool inside = __all_sync(0xffffffffu, rowok == kAll);
   auto load = [&](int q, float (&v)[R + 2]) {
-    const uint32_t ok = (q >= 0 && q < Z) ? rowok : 0u;
     const uint32_t pb = base + static_cast<uint32_t>(q) * g.XY;  // wraps for row y0-1 = -1
+    if (inside && q >= 0 && q < Z) {
 #pragma unroll
-    for (int r = 0; r < R + 2; ++r) v[r] = ((ok >> r) & 1u) ? __ldg(vals + (pb + r * X1)) : 0.f;
+      for (int r = 0; r < R + 2; ++r) v[r] = __ldg(vals + (pb + r * X1));
+    } else {
+      const uint32_t ok = (q >= 0 && q < Z) ? rowok : 0u;
+#pragma unroll
+      for (int r = 0; r < R + 2; ++r) v[r] = __ldg(vals + (((ok >> r) & 1u) ? pb + r * X1 : 0u));
+    }
   };
-  auto keys = [&](int q, const float (&v)[R + 2], uint32_t (&k)[R + 2]) {
-    const uint32_t ok = (q >= 0 && q < Z) ? rowok : 0u;
+  auto keys = [&](int q, const float (&v)[R + 2], uint32_t (&k)[R + 2], uint32_t (&dk)[R + 2]) {
+    if (inside && q >= 0 && q < Z) {
 #pragma unroll
-    for (int r = 0; r < R + 2; ++r) k[r] = ((ok >> r) & 1u) ? fkey(v[r]) : 0u;
+      for (int r = 0; r < R + 2; ++r) k[r] = fkey(v[r]);
+    } else {
+      const uint32_t ok = (q >= 0 && q < Z) ? rowok : 0u;
+#pragma unroll
+      for (int r = 0; r < R + 2; ++r) k[r] = ((ok >> r) & 1u) ? fkey(v[r]) : 0u;
+    }
+#pragma unroll
+    for (int r = 0; r < R + 2; ++r) dk[r] = k[r] - 1u;
   };
   float v[R + 2];
-  uint32_t k[R + 2];
+  uint32_t k[R + 2], dk[R + 2];
   K1Ext C[R];
   load(s0 - 1, v);
-  // q = s0-1: cells only; q = s0: cubes(s0-1) -> C; then one plane per trip
-  keys(s0 - 1, v, k);
+  // q = s0-1: cells only; q = s0: cubes(s0-1); then one plane per trip
+  keys(s0 - 1, v, k, dk);
   load(s0, v);
-  k1_plane(k, cell, C, false, false, nullptr, g.X, 0);
-  keys(s0, v, k);
+  k1_plane(k, dk, cell, C, false, false, nullptr, g.X, 0);
+  keys(s0, v, k, dk);
   load(s0 + 1, v);
-  k1_plane(k, cell, C, true, false, nullptr, g.X, 0);
+  k1_plane(k, dk, cell, C, true, false, nullptr, g.X, 0);
   uint8_t* out = dir + (base + g.X) + static_cast<uint64_t>(s0) * g.XY;  // row y0, plane s0
   for (int q = s0 + 1; q <= s1; ++q) {
-    keys(q, v, k);
+    keys(q, v, k, dk);
     load(q + 1, v);
-    k1_plane(k, cell, C, true, true, out, g.X, rows_out);
+    k1_plane(k, dk, cell, C, true, true, out, g.X, rows_out);
     out += g.XY;
   }
 }
