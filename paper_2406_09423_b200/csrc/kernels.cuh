@@ -2498,14 +2498,33 @@ __global__ void __launch_bounds__(256) k_validate(const T* __restrict__ f,
                                                   const T* __restrict__ fh, uint64_t n, double xi,
                                                   Ctl* ctl) {
   uint32_t bad = 0, viol = 0;
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += stride) {
-    const double a = static_cast<double>(__ldg(f + i));
-    const double b = static_cast<double>(__ldg(fh + i));
+  auto check = [&](T fa, T fb) {
+    const double a = static_cast<double>(fa), b = static_cast<double>(fb);
     if (!isfinite(a) || !isfinite(b)) ++bad;
     else if (fabs(__dsub_rn(a, b)) > xi) ++viol;
+  };
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  uint64_t head = 0;
+  if (sizeof(T) == 4 && ((reinterpret_cast<uintptr_t>(f) | reinterpret_cast<uintptr_t>(fh)) & 15u) == 0) {
+    // f32, 16-byte aligned (slab windows may not be): two 16-byte loads per array in flight
+    const uint64_t n4 = n / 4;
+    const float4* f4 = reinterpret_cast<const float4*>(f);
+    const float4* h4 = reinterpret_cast<const float4*>(fh);
+    for (uint64_t i = t0; i < n4; i += 2 * stride) {
+      const bool two = i + stride < n4;
+      const float4 a0 = __ldg(f4 + i), b0 = __ldg(h4 + i);
+      float4 a1 = a0, b1 = b0;
+      if (two) {
+        a1 = __ldg(f4 + i + stride);
+        b1 = __ldg(h4 + i + stride);
+      }
+      check(a0.x, b0.x), check(a0.y, b0.y), check(a0.z, b0.z), check(a0.w, b0.w);
+      if (two) check(a1.x, b1.x), check(a1.y, b1.y), check(a1.z, b1.z), check(a1.w, b1.w);
+    }
+    head = n4 * 4;
   }
+  for (uint64_t i = head + t0; i < n; i += stride) check(__ldg(f + i), __ldg(fh + i));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     bad += __shfl_xor_sync(0xffffffffu, bad, o);
