@@ -79,6 +79,27 @@ def test_directions_labels_vs_oracle(P, oracle_lib, dims, dt):
         assert np.array_equal(lab.max_label, M) and np.array_equal(lab.min_label, m)
 
 
+@pytest.mark.parametrize("dims", [[31, 7, 9], [32, 64, 3], [33, 65, 17], [61, 60, 59], [1000, 3, 11],
+                                  [3, 1000, 11], [130, 129, 2], [2, 2, 2]])
+def test_k1_columns_vs_oracle_and_smem_k1(P, oracle_lib, dims, monkeypatch):
+    """The 3D f32 K1 (k_directions_col3: 30-column warps, 8-row strips, z
+    chunks) at column/row/plane boundaries, against the oracle and against the
+    shared-memory K1 (k_directions_reg3, MSSZ_K1_REG3=1)."""
+    rng = np.random.default_rng(11)
+    topo = P.build_topology(dims)
+    n = topo.vertex_count
+    for vals in (rng.integers(-2, 3, n).astype(np.float32),
+                 rng.choice(np.array([0.0, -0.0, 1.0, -1.0], np.float32), n),
+                 rng.standard_normal(n).astype(np.float32)):
+        codes = P.compute_direction_codes(topo, vals)
+        d = P.compute_directions(topo, vals)
+        a, b = oracle_lib.compute_directions(dims, vals)
+        assert np.array_equal(d.asc, a) and np.array_equal(d.desc, b)
+        monkeypatch.setenv("MSSZ_K1_REG3", "1")
+        assert np.array_equal(P.compute_direction_codes(topo, vals), codes)
+        monkeypatch.delenv("MSSZ_K1_REG3")
+
+
 def test_signed_zero_ties(P):
     vals = np.array([0.0, -0.0] * 8, np.float32)
     topo = P.build_topology([4, 4])
