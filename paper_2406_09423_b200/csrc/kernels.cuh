@@ -1715,22 +1715,26 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
     }
   }
   __syncthreads();
-  // local parents; a chain that leaves the tile stops at its last inside vertex
+  // local parents; a chain that leaves the tile stops at its last inside vertex.
+  // Element i = tid + j*kLabelTileThreads: its column is a per-thread constant
+  // (and in 3D its row too), so most of the face mask is computed once.
   uint32_t own[PER];
+  const int lx0 = threadIdx.x & (TL::TX - 1);
+  const uint32_t onx = (lx0 == 0 ? 1u : 0u) | (lx0 == ex - 1 ? 2u : 0u);
 #pragma unroll
   for (int j = 0; j < PER; ++j) {
     const int i = threadIdx.x + j * kLabelTileThreads;
-    const int lx = i & (TL::TX - 1), ly = (i >> TL::LX) & (TL::TY - 1), lz = i >> (TL::LX + TL::LY);
+    const int ly = (i >> TL::LX) & (TL::TY - 1), lz = i >> (TL::LX + TL::LY);
     const uint32_t code = sdir[i];
     // faces of the (partial) tile this element lies on; outside elements stay put
-    const uint32_t on = (lx < ex && ly < ey && lz < ez)
-                            ? ((lx == 0 ? 1u : 0u) | (lx == ex - 1 ? 2u : 0u) | (ly == 0 ? 4u : 0u) |
-                               (ly == ey - 1 ? 8u : 0u) | (lz == 0 ? 16u : 0u) | (lz == ez - 1 ? 32u : 0u))
-                            : 63u;
+    const uint32_t ony = (ly == 0 ? 4u : 0u) | (ly == ey - 1 ? 8u : 0u);
+    const uint32_t onz = (lz == 0 ? 16u : 0u) | (lz == ez - 1 ? 32u : 0u);
+    const bool inside = lx0 < ex && ly < ey && lz < ez;
+    const uint32_t on = inside ? (onx | ony | onz) : 63u;
     const uint2 e = scode[code];  // SELF: offset 0, no face
     const uint32_t pa = (e.y & on) ? i : i + static_cast<int32_t>(static_cast<int16_t>(e.x & 0xFFFFu));
     const uint32_t pd = ((e.y >> 8) & on) ? i : i + (static_cast<int32_t>(e.x) >> 16);
-    own[j] = pa | (pd << 16);
+    own[j] = 4 * pa | ((4 * pd) << 16);  // byte offsets of the parents' words (< 2^15)
     ptr[i] = own[j];
   }
   __syncthreads();
@@ -1750,7 +1754,10 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
     for (int j = 0; j < PER; ++j) {
       const int i = threadIdx.x + j * kLabelTileThreads;
       const uint32_t p = own[j];
-      const uint32_t np = (ptr[p & 0xFFFFu] & 0xFFFFu) | (ptr[p >> 16] & 0xFFFF0000u);
+      // the asc half of the word at byte offset p & 0xFFFF, the desc half of the one at p >> 16
+      const uint32_t np = *reinterpret_cast<const uint16_t*>(reinterpret_cast<const uint8_t*>(ptr) + (p & 0xFFFFu)) |
+                          (static_cast<uint32_t>(*reinterpret_cast<const uint16_t*>(
+                               reinterpret_cast<const uint8_t*>(ptr) + (p >> 16) + 2)) << 16);
       if (np != p) {
         own[j] = np;
         ptr[i] = np;
@@ -1771,7 +1778,7 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
       const uint32_t gi = base + lx + g.X * ly + g.XY * lz;
 #pragma unroll
       for (int fam = 0; fam < 2; ++fam) {
-        const int t = fam ? (p >> 16) : (p & 0xFFFFu);
+        const int t = (fam ? (p >> 16) : (p & 0xFFFFu)) >> 2;
         const uint32_t c = (sdir[t] >> (4 * fam)) & 15u;
         const uint32_t res = base + (t & (TL::TX - 1)) + g.X * ((t >> TL::LX) & (TL::TY - 1)) +
                              g.XY * (t >> (TL::LX + TL::LY)) + soff[c];
