@@ -1769,24 +1769,34 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
   // provisional labels (root, or first vertex outside the tile) + the exits:
   // the chain's last inside vertex t is a root (code SELF) or steps out by
   // slot c, so the label is gid(t) + soff[c] (soff[SELF] = 0)
+  // element j of this thread: gid = gi0 + j * jstride (its column, and in 3D
+  // its row, are per-thread constants; a j step is RPJ rows)
+  constexpr int RPJ = kLabelTileThreads / TL::TX;
+  const uint32_t gi0 = base + lx0 + g.X * ((threadIdx.x >> TL::LX) & (TL::TY - 1)) +
+                       g.XY * (threadIdx.x >> (TL::LX + TL::LY));
+  const uint32_t jstride = DIM == 3 ? g.XY * (RPJ / TL::TY) : g.X * RPJ;
+  auto label_one = [&](uint32_t p, uint32_t gi) {
 #pragma unroll
-  for (int j = 0; j < PER; ++j) {
-    const int i = threadIdx.x + j * kLabelTileThreads;
-    const int lx = i & (TL::TX - 1), ly = (i >> TL::LX) & (TL::TY - 1), lz = i >> (TL::LX + TL::LY);
-    if (lx < ex && ly < ey && lz < ez) {
-      const uint32_t p = own[j];
-      const uint32_t gi = base + lx + g.X * ly + g.XY * lz;
+    for (int fam = 0; fam < 2; ++fam) {
+      const int t = (fam ? (p >> 16) : (p & 0xFFFFu)) >> 2;
+      const uint32_t c = (sdir[t] >> (4 * fam)) & 15u;
+      const uint32_t res = base + (t & (TL::TX - 1)) + g.X * ((t >> TL::LX) & (TL::TY - 1)) +
+                           g.XY * (t >> (TL::LX + TL::LY)) + soff[c];
+      (fam ? m : M)[gi] = res;
+      // fin is only ever read at provisional-label values: roots (here) and
+      // exits (seeded by k_exit_reset), so non-roots need no fin write
+      if (res == gi) (fam ? finm : finM)[gi] = res;
+    }
+  };
+  if (full) {
 #pragma unroll
-      for (int fam = 0; fam < 2; ++fam) {
-        const int t = (fam ? (p >> 16) : (p & 0xFFFFu)) >> 2;
-        const uint32_t c = (sdir[t] >> (4 * fam)) & 15u;
-        const uint32_t res = base + (t & (TL::TX - 1)) + g.X * ((t >> TL::LX) & (TL::TY - 1)) +
-                             g.XY * (t >> (TL::LX + TL::LY)) + soff[c];
-        (fam ? m : M)[gi] = res;
-        // fin is only ever read at provisional-label values: roots (here) and
-        // exits (seeded by k_exit_reset), so non-roots need no fin write
-        if (res == gi) (fam ? finm : finM)[gi] = res;
-      }
+    for (int j = 0; j < PER; ++j) label_one(own[j], gi0 + j * jstride);
+  } else {
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int i = threadIdx.x + j * kLabelTileThreads;
+      const int ly = (i >> TL::LX) & (TL::TY - 1), lz = i >> (TL::LX + TL::LY);
+      if (lx0 < ex && ly < ey && lz < ez) label_one(own[j], gi0 + j * jstride);
     }
   }
   // the tile's distinct exits: only surface elements can step out, so walk the
