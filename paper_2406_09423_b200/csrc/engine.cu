@@ -22,6 +22,7 @@
 
 #include "../../include/mssz_cuda.h"
 #include "kernels.cuh"
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
 
 namespace mssz_b200 {
 namespace {
@@ -74,6 +75,35 @@ int guarded(F&& body) {
 }
 
 // Validates dims like build_topology (grid.cpp:39-55) plus the u32 id limit.
+// TMA descriptor of a 3D direction field for k_label_tile's 32x16x16-byte tile
+// loads (cuTensorMapEncodeTiled through the runtime's driver entry point).
+// false (byte/vector loads instead): 2D, strides not 16-byte multiples, no
+// driver entry point, or MSSZ_LABEL_TMA=0.
+bool label_tile_map(const Geom& g, const uint8_t* dir, CUtensorMap* map) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  std::memset(map, 0, sizeof(*map));
+  if (const char* e = std::getenv("MSSZ_LABEL_TMA"))
+    if (std::atoi(e) == 0) return false;
+  using TL = LabelTile<3>;
+  if (!enc || g.ndims != 3 || g.X % 16 || g.XY % 16 || reinterpret_cast<uintptr_t>(dir) % 16 || g.X < TL::TX ||
+      g.Y < TL::TY || g.Z < TL::TZ)
+    return false;
+  const cuuint64_t gdim[3] = {g.X, g.Y, g.Z};
+  const cuuint64_t gstride[2] = {g.X, static_cast<cuuint64_t>(g.XY)};
+  const cuuint32_t box[3] = {TL::TX, TL::TY, TL::TZ};
+  const cuuint32_t estride[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(dir), gdim, gstride, box, estride,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 Geom make_geom(int ndims, const uint64_t* dims) {
   if (ndims != 2 && ndims != 3) fail(MSSZ_CU_ERR_USAGE, "dims must have 2 or 3 extents");
   if (!dims) fail(MSSZ_CU_ERR_USAGE, "dims is null");
@@ -570,12 +600,14 @@ struct Engine {
     if (ntodo) {
       CK(cudaMemsetAsync(ts.err, 0, sizeof(uint32_t), ws.stream));
       pre(kProfLabelInit);
+      CUtensorMap dmap;
+      const int use_tma = label_tile_map(geo, dir, &dmap) ? 1 : 0;
       if (geo.ndims == 2)
         k_label_tile<2><<<ntodo, kLabelTileThreads, label_tile_smem<2>(), ws.stream>>>(
-            dir, geo, M, m, fM, fm, list, ts);
+            dir, geo, M, m, fM, fm, list, ts, dmap, 0);
       else
         k_label_tile<3><<<ntodo, kLabelTileThreads, label_tile_smem<3>(), ws.stream>>>(
-            dir, geo, M, m, fM, fm, list, ts);
+            dir, geo, M, m, fM, fm, list, ts, dmap, use_tma);
       launched(kProfLabelInit);
     }
     st.label_tiles += ntodo;

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cooperative_groups.h>
+#include <cuda.h>  // CUtensorMap (TMA descriptor of the direction field)
 
 #include "common.cuh"
 
@@ -1628,7 +1629,7 @@ template <int DIM>
 __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
     const uint8_t* __restrict__ dir, Geom g, uint32_t* __restrict__ M, uint32_t* __restrict__ m,
     uint32_t* __restrict__ finM, uint32_t* __restrict__ finm, const uint32_t* tile_list,
-    TileStore ts) {
+    TileStore ts, const __grid_constant__ CUtensorMap dmap, int use_tma) {
   using TL = LabelTile<DIM>;
   constexpr int NS = StencilSize<DIM>::value;
   constexpr int PER = kLabelTileN / kLabelTileThreads;
@@ -1636,7 +1637,7 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
   //   ptr   u32[kLabelTileN]  (asc local parent) | (desc local parent) << 16
   //   sexit u32[2][kSurface]  exits can only leave from the tile surface
   //   sdir  u8[kLabelTileN]
-  extern __shared__ __align__(16) uint8_t label_smem[];
+  extern __shared__ __align__(128) uint8_t label_smem[];  // sdir at a 128-byte multiple: a TMA destination
   uint32_t* ptr = reinterpret_cast<uint32_t*>(label_smem);
   uint32_t (*sexit)[LabelTile<DIM>::kSurface] =
       reinterpret_cast<uint32_t (*)[LabelTile<DIM>::kSurface]>(ptr + kLabelTileN);
@@ -1658,7 +1659,9 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
 #pragma unroll
     for (int k = 0; k < NS; ++k)
       if (k == static_cast<int>(threadIdx.x)) stencil<DIM>(k, dx, dy, dz);
-    soff[threadIdx.x] = g.off[threadIdx.x];
+    // = g.off[k] (mod 2^32), without a dynamically indexed kernel parameter
+    soff[threadIdx.x] = static_cast<int32_t>(static_cast<uint32_t>(dx) + static_cast<uint32_t>(dy) * g.X +
+                                             static_cast<uint32_t>(dz) * g.XY);
     sface[threadIdx.x] = (dx < 0 ? 1u : 0u) | (dx > 0 ? 2u : 0u) | (dy < 0 ? 4u : 0u) | (dy > 0 ? 8u : 0u) |
                          (dz < 0 ? 16u : 0u) | (dz > 0 ? 32u : 0u);
     shalo[threadIdx.x] = dx + (TL::TX + 2) * (dy + (TL::TY + 2) * dz);
@@ -1693,8 +1696,38 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
   const int ez = DIM == 2 ? 1 : min(TL::TZ, static_cast<int>(g.Z - z0));
   const uint32_t base = x0 + g.X * y0 + g.XY * z0;
   const bool full = ex == TL::TX && ey == TL::TY && ez == TL::TZ;
-  // dir tile: 16-byte vector loads when rows are 16-byte aligned and whole
-  if (full && (g.X % 16) == 0) {
+  // dir tile of a whole 3D tile inside the owned range: one TMA box load
+  // (cp.async.bulk.tensor.3d, 32x16x16 bytes in the tile's own element order)
+  // completing on an mbarrier; otherwise 16-byte vector loads when rows are
+  // 16-byte aligned and whole, else byte loads with out-of-range fill
+  const bool tma = DIM == 3 && use_tma && full && base >= ts.own_lo &&
+                   base + (TL::TX - 1) + g.X * (TL::TY - 1) + g.XY * (TL::TZ - 1) < ts.own_hi;
+  if (tma) {
+    __shared__ __align__(8) uint64_t tbar;
+    const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&tbar));
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kLabelTileN)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+              static_cast<uint32_t>(__cvta_generic_to_shared(sdir))),
+          "l"(reinterpret_cast<uint64_t>(&dmap)), "r"(x0), "r"(y0), "r"(z0), "r"(bar)
+          : "memory");
+    }
+    __syncthreads();  // the barrier is initialised before anyone waits on it
+    uint32_t done = 0;
+    for (uint32_t it = 0; !done; ++it) {
+      asm volatile(
+          "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}"
+          : "=r"(done)
+          : "r"(bar)
+          : "memory");
+      if (it > (1u << 22)) __trap();  // a lost transfer fails the launch instead of hanging it
+    }
+  } else if (full && (g.X % 16) == 0) {
     constexpr int VPR = TL::TX / 16;  // uint4 per row
     for (int q = threadIdx.x; q < kLabelTileN / 16; q += kLabelTileThreads) {
       const int row = q / VPR, c = q % VPR;

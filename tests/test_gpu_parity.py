@@ -100,6 +100,26 @@ def test_k1_columns_vs_oracle_and_smem_k1(P, oracle_lib, dims, monkeypatch):
         monkeypatch.delenv("MSSZ_K1_REG3")
 
 
+@pytest.mark.parametrize("dims", [[64, 48, 40], [96, 32, 33], [32, 16, 16], [48, 17, 31], [40, 20, 18]])
+def test_label_tile_tma_vs_vector_loads(P, oracle_lib, dims, monkeypatch):
+    """k_label_tile loads whole in-range 3D tiles with one TMA box
+    (cp.async.bulk.tensor.3d on an mbarrier) when the field's strides allow it;
+    labels must equal the vector-load path (MSSZ_LABEL_TMA=0) and the oracle,
+    including partial tiles and fields whose strides rule TMA out."""
+    from paper_2406_09423_b200 import inputs as I
+    rng = np.random.default_rng(5)
+    topo = P.build_topology(dims)
+    for vals in (I.generate("random-smooth", dims, 3, np.float32),
+                 rng.integers(0, 7, topo.vertex_count).astype(np.float32)):
+        lab = P.segmentation(topo, vals)
+        a, b = oracle_lib.compute_directions(dims, vals)
+        M, m = oracle_lib.compute_labels(dims, a, b)
+        assert np.array_equal(lab.max_label, M) and np.array_equal(lab.min_label, m)
+        monkeypatch.setenv("MSSZ_LABEL_TMA", "0")
+        assert P.segmentation(topo, vals) == lab
+        monkeypatch.delenv("MSSZ_LABEL_TMA")
+
+
 def test_signed_zero_ties(P):
     vals = np.array([0.0, -0.0] * 8, np.float32)
     topo = P.build_topology([4, 4])
