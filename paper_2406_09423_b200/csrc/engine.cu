@@ -370,6 +370,7 @@ struct Engine {
   std::vector<T> host_g;  // on_batch snapshots only
   bool trace = std::getenv("MSSZ_TRACE") != nullptr;  // per-iteration log on stderr
   bool k1_reg3 = std::getenv("MSSZ_K1_REG3") != nullptr;  // A/B: the shared-memory K1 (k_directions_reg3)
+  bool exit_reset_forced = std::getenv("MSSZ_EXIT_RESET") != nullptr;  // A/B: k_exit_reset on full label passes
   uint64_t r_last_mism = ~uint64_t(0);  // mismatches of the latest R iteration
   bool r_full_valid = false;            // tile label state matches gdir (no C edits since)
   bool x_valid = false;                 // crossing lists X match gdir (for k_cross_update)
@@ -597,6 +598,10 @@ struct Engine {
       ntodo = select_tiles(ts, 0, 0);
       list = tile_list(0);
     }
+    // a pass over every tile seeds the exits' fin entries itself (k_label_tile
+    // writes fin on tile surfaces), so k_exit_reset is skipped; an incremental
+    // pass keeps save -> reset so changed exit finals are detected
+    const bool seed_exits = !only_dirty && !exit_reset_forced;
     if (ntodo) {
       CK(cudaMemsetAsync(ts.err, 0, sizeof(uint32_t), ws.stream));
       pre(kProfLabelInit);
@@ -604,10 +609,10 @@ struct Engine {
       const int use_tma = label_tile_map(geo, dir, &dmap) ? 1 : 0;
       if (geo.ndims == 2)
         k_label_tile<2><<<ntodo, kLabelTileThreads, label_tile_smem<2>(), ws.stream>>>(
-            dir, geo, M, m, fM, fm, list, ts, dmap, 0);
+            dir, geo, M, m, fM, fm, list, ts, dmap, 0, seed_exits ? 1 : 0);
       else
         k_label_tile<3><<<ntodo, kLabelTileThreads, label_tile_smem<3>(), ws.stream>>>(
-            dir, geo, M, m, fM, fm, list, ts, dmap, use_tma);
+            dir, geo, M, m, fM, fm, list, ts, dmap, use_tma, seed_exits ? 1 : 0);
       launched(kProfLabelInit);
     }
     st.label_tiles += ntodo;
@@ -619,9 +624,11 @@ struct Engine {
       k_exit_save<<<ts.ntiles, 256, 0, ws.stream>>>(ts, fM, fm);
       launched(kProfLabelJump);
     }
-    pre(kProfLabelJump);
-    k_exit_reset<<<ts.ntiles, 256, 0, ws.stream>>>(ts, M, m, fM, fm);
-    launched(kProfLabelJump);
+    if (!seed_exits) {
+      pre(kProfLabelJump);
+      k_exit_reset<<<ts.ntiles, 256, 0, ws.stream>>>(ts, M, m, fM, fm);
+      launched(kProfLabelJump);
+    }
     uint32_t* cnt[2] = {&ws.ctl->s_count, &ws.ctl->list_count[0]};  // (asc, desc) pairs
     uint32_t* la[2] = {list_ptr(2), list_ptr(0)};
     uint32_t* ld[2] = {list_ptr(3), list_ptr(1)};

@@ -1629,7 +1629,7 @@ template <int DIM>
 __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
     const uint8_t* __restrict__ dir, Geom g, uint32_t* __restrict__ M, uint32_t* __restrict__ m,
     uint32_t* __restrict__ finM, uint32_t* __restrict__ finm, const uint32_t* tile_list,
-    TileStore ts, const __grid_constant__ CUtensorMap dmap, int use_tma) {
+    TileStore ts, const __grid_constant__ CUtensorMap dmap, int use_tma, int seed_exits) {
   using TL = LabelTile<DIM>;
   constexpr int NS = StencilSize<DIM>::value;
   constexpr int PER = kLabelTileN / kLabelTileThreads;
@@ -1808,7 +1808,12 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
   const uint32_t gi0 = base + lx0 + g.X * ((threadIdx.x >> TL::LX) & (TL::TY - 1)) +
                        g.XY * (threadIdx.x >> (TL::LX + TL::LY));
   const uint32_t jstride = DIM == 3 ? g.XY * (RPJ / TL::TY) : g.X * RPJ;
-  auto label_one = [&](uint32_t p, uint32_t gi) {
+  // fin is only ever read at provisional-label values: roots and exits.  Roots
+  // are written here.  Every exit is a surface element of the tile it lies in
+  // (a chain leaves a tile by one stencil step), so with seed_exits (a pass
+  // over every tile) surface elements also write fin = their provisional label
+  // -- what k_exit_reset would copy there -- and that launch is skipped.
+  auto label_one = [&](uint32_t p, uint32_t gi, bool surf) {
 #pragma unroll
     for (int fam = 0; fam < 2; ++fam) {
       const int t = (fam ? (p >> 16) : (p & 0xFFFFu)) >> 2;
@@ -1816,20 +1821,26 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
       const uint32_t res = base + (t & (TL::TX - 1)) + g.X * ((t >> TL::LX) & (TL::TY - 1)) +
                            g.XY * (t >> (TL::LX + TL::LY)) + soff[c];
       (fam ? m : M)[gi] = res;
-      // fin is only ever read at provisional-label values: roots (here) and
-      // exits (seeded by k_exit_reset), so non-roots need no fin write
-      if (res == gi) (fam ? finm : finM)[gi] = res;
+      if (res == gi || surf) (fam ? finm : finM)[gi] = res;
     }
+  };
+  const bool sx = seed_exits && onx != 0;
+  auto surface = [&](int ly, int lz) {
+    return seed_exits && (sx || ly == 0 || ly == ey - 1 || lz == 0 || lz == ez - 1);
   };
   if (full) {
 #pragma unroll
-    for (int j = 0; j < PER; ++j) label_one(own[j], gi0 + j * jstride);
+    for (int j = 0; j < PER; ++j) {
+      const int i = threadIdx.x + j * kLabelTileThreads;
+      const int ly = (i >> TL::LX) & (TL::TY - 1), lz = i >> (TL::LX + TL::LY);
+      label_one(own[j], gi0 + j * jstride, surface(ly, lz));
+    }
   } else {
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
       const int i = threadIdx.x + j * kLabelTileThreads;
       const int ly = (i >> TL::LX) & (TL::TY - 1), lz = i >> (TL::LX + TL::LY);
-      if (lx0 < ex && ly < ey && lz < ez) label_one(own[j], gi0 + j * jstride);
+      if (lx0 < ex && ly < ey && lz < ez) label_one(own[j], gi0 + j * jstride, surface(ly, lz));
     }
   }
   // the tile's distinct exits: only surface elements can step out, so walk the
