@@ -665,7 +665,7 @@ __device__ __forceinline__ K1Ext k1_join(const K1Ext& lo, const K1Ext& hi, uint3
 
 __device__ __forceinline__ K1Ext k1_xpair(uint32_t k, uint32_t dk) {  // (x, x+1) of one row
   const uint32_t k1 = __shfl_down_sync(0xffffffffu, k, 1);
-  const uint32_t dk1 = __shfl_down_sync(0xffffffffu, dk, 1);
+  const uint32_t dk1 = k1 - 1u;  // one shuffle: the shuffle pipe is shared with L1/shared
   K1Ext r;
   const bool ta = k1 >= k;
   r.ak = ta ? k1 : k;
