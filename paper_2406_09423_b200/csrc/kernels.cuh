@@ -1601,7 +1601,7 @@ constexpr int kLabelTileN = 8192;
 constexpr int kLabelTileThreads = 512;
 template <int DIM>
 constexpr size_t label_tile_smem() {
-  return kLabelTileN * 4 + 2 * LabelTile<DIM>::kSurface * 4 + kLabelTileN;
+  return kLabelTileN * 4 + kLabelTileN;  // 40 KB: four 512-thread CTAs per SM
 }
 
 // Per-tile label state kept across R-loop iterations (incremental labels).
@@ -1635,13 +1635,11 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
   constexpr int PER = kLabelTileN / kLabelTileThreads;
   // dynamic shared memory (label_tile_smem<DIM>() bytes):
   //   ptr   u32[kLabelTileN]  (asc local parent) | (desc local parent) << 16
-  //   sexit u32[2][kSurface]  exits can only leave from the tile surface
   //   sdir  u8[kLabelTileN]
+  // (the tile's distinct exits go straight to its tile-store slots, ts.E)
   extern __shared__ __align__(128) uint8_t label_smem[];  // sdir at a 128-byte multiple: a TMA destination
   uint32_t* ptr = reinterpret_cast<uint32_t*>(label_smem);
-  uint32_t (*sexit)[LabelTile<DIM>::kSurface] =
-      reinterpret_cast<uint32_t (*)[LabelTile<DIM>::kSurface]>(ptr + kLabelTileN);
-  uint8_t* sdir = reinterpret_cast<uint8_t*>(ptr + kLabelTileN + 2 * LabelTile<DIM>::kSurface);
+  uint8_t* sdir = reinterpret_cast<uint8_t*>(ptr + kLabelTileN);
   __shared__ uint32_t sexit_n[2];
   // per-family bitmap over the tile's halo box: each distinct exit is listed once per tile
   constexpr int HBOX = (TL::TX + 2) * (TL::TY + 2) * (DIM == 2 ? 1 : TL::TZ + 2);
@@ -1880,17 +1878,13 @@ __global__ void __launch_bounds__(kLabelTileThreads) k_label_tile(
         if (!(sface[c] & on)) continue;  // SELF or a step inside the tile
         const int h = hb + shalo[c];
         if (!(atomicOr(&seen[fam][h >> 5], 1u << (h & 31)) & (1u << (h & 31))))
-          sexit[fam][atomicAdd(&sexit_n[fam], 1u)] = gi + soff[c];
+          ts.E[(static_cast<size_t>(b) * 2 + fam) * LabelTile<DIM>::kSurface + atomicAdd(&sexit_n[fam], 1u)] =
+              gi + soff[c];
       }
     }
   }
   __syncthreads();
-#pragma unroll
-  for (int fam = 0; fam < 2; ++fam) {
-    uint32_t* E = ts.E + (static_cast<size_t>(b) * 2 + fam) * LabelTile<DIM>::kSurface;
-    for (uint32_t k = threadIdx.x; k < sexit_n[fam]; k += kLabelTileThreads) E[k] = sexit[fam][k];
-    if (threadIdx.x == 0) ts.Ecnt[b * 2 + fam] = sexit_n[fam];
-  }
+  if (threadIdx.x < 2) ts.Ecnt[b * 2 + threadIdx.x] = sexit_n[threadIdx.x];
 }
 
 // Phase 2a (all tiles): remember every exit's final label (k_exit_save), then
