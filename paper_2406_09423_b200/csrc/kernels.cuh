@@ -887,6 +887,9 @@ constexpr uint32_t kParked = 0xFFFFFFFFu;
 #define MSSZ_FIX_PER_LANE 2
 #endif
 constexpr int kFixPerLane = MSSZ_FIX_PER_LANE;
+#ifndef MSSZ_FIX_LIST_PER_LANE
+#define MSSZ_FIX_LIST_PER_LANE 4
+#endif
 
 // claim (edit_engine.cpp:160-169) + lower_step (:75-86): the first claimant of
 // t in this batch lowers it from the pre-batch value; exactly one winner per
@@ -905,14 +908,13 @@ __device__ __forceinline__ bool claim_and_lower(const State<T>& s, uint32_t t, u
 // (claim lost, or target at its floor).  Every other item is a neighbour of
 // (or is) a lowered target, hence in this batch's frontier, and is
 // re-evaluated there; only retry items need the old-list membership test.
-template <class T>
+template <class T, int J = kFixPerLane>
 __device__ __forceinline__ void fix_batch(const State<T>& s, const uint32_t* __restrict__ list,
                                           uint32_t n, int rule, uint32_t batch, uint32_t* s_count,
                                           uint64_t tid, uint64_t stride, uint32_t* retry = nullptr,
                                           uint32_t* retry_count = nullptr, uint32_t* park = nullptr,
                                           uint32_t* park_count = nullptr) {
   // J list items per lane per step: their loads and claims overlap
-  constexpr int J = kFixPerLane;
   const uint64_t step = J * stride;
   __shared__ uint32_t sstage[kStageWarps][kStageK * 32], rstage[kStageWarps][kStageK * 32];
   WarpBuffer<kStageK> sbuf(warp_stage(sstage)), rbuf(warp_stage(rstage));
@@ -1173,7 +1175,8 @@ __device__ __forceinline__ void detect_chunks(const uint8_t* __restrict__ fdir,
 template <class T>
 __global__ void __launch_bounds__(256) k_fix_list(State<T> s, const uint32_t* __restrict__ list,
                                                   uint32_t n, int rule, uint32_t batch) {
-  fix_batch(s, list, n, rule, batch, &s.ctl->s_count,
+  // standalone list fix (R batches, huge C batches): four items per lane in flight
+  fix_batch<T, MSSZ_FIX_LIST_PER_LANE>(s, list, n, rule, batch, &s.ctl->s_count,
             static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x,
             static_cast<uint64_t>(gridDim.x) * blockDim.x);
 }
